@@ -1,0 +1,70 @@
+"""Shared test plumbing.
+
+Markers: ``gpu`` -- needs a B200 (run with ``-m gpu``); everything else
+runs on CPU.  The golden fixtures under tests/golden/ were produced from
+the reference itself by tests/golden/make_golden.py.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device")
+
+
+def load_cases(name):
+    """Return a list of dicts (one per case) from tests/golden/<name>.npz."""
+    data = np.load(os.path.join(GOLDEN, name))
+    cases = {}
+    for key in data.files:
+        idx, field = key.split("_", 1)
+        cases.setdefault(int(idx[1:]), {})[field] = data[key]
+    meta_path = os.path.join(GOLDEN, name.replace(".npz", ".json"))
+    meta = json.load(open(meta_path)) if os.path.exists(meta_path) else {}
+    out = []
+    for i in sorted(cases):
+        c = cases[i]
+        if "cases" in meta:
+            c["meta"] = meta["cases"][i]
+        out.append(c)
+    return out
+
+
+@pytest.fixture(scope="session")
+def selection_golden():
+    return load_cases("selection.npz")
+
+
+@pytest.fixture(scope="session")
+def remap_golden():
+    return load_cases("remap.npz")
+
+
+@pytest.fixture(scope="session")
+def forward_golden():
+    return load_cases("forward.npz")
+
+
+@pytest.fixture
+def rng():
+    return np.random.default_rng(1234)
+
+
+def has_gpu() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
