@@ -1,0 +1,215 @@
+/*
+ * lynx_b200.h -- C ABI of the B200-native Lynx MoE decode hot path.
+ *
+ * The reference (moetrim, /root/reference/pkg/src/moetrim) is a pure-Python
+ * package with no FFI; its "operator API" for this path is three Python
+ * calls, which this library replaces one-for-one:
+ *
+ *   route_batch(logits, k)                    router.py:174-187
+ *   apply_policy(selection, phase, config)    policy.py:341-350
+ *     (latency_policy 232-264, accuracy_policy 287-338,
+ *      remap_tokens 151-212, full_retain_mask 215-229)
+ *   forward_layer(hidden, model, layer, mask) simulator.py:86-113
+ *     (router_logits 82-83, rms_norm 26-27, expert_mlp 77-79)
+ *
+ * Python binds these entry points with ctypes
+ * (paper_2411_08982_b200/_native.py); INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer owned by the caller,
+ *     except the const struct pointers (lynx_policy_t, lynx_layer_t,
+ *     lynx_selection_t, lynx_dispatch_t), which are host structs holding
+ *     device pointers.  The library never allocates or frees and keeps no
+ *     global mutable state; calls are re-entrant and stream-ordered.
+ *   - bf16 tensors are passed as uint16_t* (raw bfloat16 bits).
+ *   - Return value: LYNX_OK (0) or a negative lynx_status.  Preconditions
+ *     the reference rejects with ValidationError map to distinct codes;
+ *     data-dependent conditions found on the device (non-finite logits,
+ *     zero probability mass, clipped drop) are reported through the
+ *     caller's int32 `flags` word, read back only when the caller asks.
+ *   - No host synchronisation inside any call; all calls are capturable
+ *     into CUDA graphs.
+ *   - Build target: sm_100a only (B200).
+ */
+#ifndef LYNX_B200_H
+#define LYNX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *lynx_stream_t; /* == cudaStream_t */
+
+enum lynx_status {
+  LYNX_OK = 0,
+  LYNX_ERR_SHAPE = -1,         /* bad T/N/d/ff, RoutingLogits shape (router.py:67-70) */
+  LYNX_ERR_TOPK = -2,          /* k outside [1, N] (router.py:176-179) */
+  LYNX_ERR_MIN_EXPERTS = -3,   /* min_experts < top_k (policy.py:61-64) */
+  LYNX_ERR_RETAINED = -4,      /* empty / out-of-range retained (policy.py:164-167) */
+  LYNX_ERR_TOKENS = -5,        /* mask/hidden token mismatch (simulator.py:97-100) */
+  LYNX_ERR_CUDA = -6,          /* a CUDA launch or driver call failed */
+  LYNX_ERR_UNSUPPORTED = -7,   /* shape outside this build's limits (see LYNX_MAX_*) */
+  LYNX_ERR_WORKSPACE = -8,     /* workspace smaller than lynx_*_workspace_bytes() */
+  LYNX_ERR_CONFIG = -9         /* invalid PolicyConfig field (policy.py:40-55) */
+};
+
+/* Device flag bits (int32 word written by the selection kernel). */
+#define LYNX_FLAG_CLIPPED 1      /* ExpertMask.clipped (policy.py:100, 250-251, 337) */
+#define LYNX_FLAG_NONFINITE 2    /* logits contain NaN/Inf (router.py:71-72) */
+#define LYNX_FLAG_ZERO_MASS 4    /* token has zero mass on assigned experts (policy.py:206-209) */
+
+/* Build limits. */
+#define LYNX_MAX_EXPERTS 64
+#define LYNX_MAX_TOPK 8
+#define LYNX_MAX_TOKENS 4096
+#define LYNX_SEG_ROWS 256        /* max token rows one expert segment feeds one MMA */
+
+enum lynx_policy_mode { LYNX_POLICY_NONE = 0, LYNX_POLICY_LATENCY = 1, LYNX_POLICY_ACCURACY = 2 };
+enum lynx_conf_metric { LYNX_CONF_TOP1 = 0, LYNX_CONF_MARGIN = 1 };
+enum lynx_activation { LYNX_ACT_SWIGLU = 0, LYNX_ACT_TANH2 = 1 };
+
+/* PolicyConfig (policy.py:26-37).  mode NONE = full_retain_mask. */
+typedef struct lynx_policy {
+  int32_t mode;
+  int32_t drop_count;
+  double confidence_threshold;
+  int32_t sample_threshold;
+  int32_t min_experts;        /* 0 = unset -> resolves to top_k (policy.py:57-65) */
+  int32_t freq_keep_budget;
+  int32_t confidence_metric;  /* lynx_conf_metric */
+  int32_t n_rank_weights;     /* 0 = one vote per slot, else == top_k */
+  int32_t reserved;
+  double rank_weights[LYNX_MAX_TOPK];
+} lynx_policy_t;
+
+/* ExpertSelection + ExpertMask outputs (router.py:84-123, policy.py:83-113).
+ * Any pointer except expert_ids/assigned/weights/flags may be NULL. */
+typedef struct lynx_selection {
+  int32_t *expert_ids;  /* [T,k] rank order, ties -> smaller index */
+  double *probs;        /* [T,k] */
+  double *full_probs;   /* [T,N] float64 softmax */
+  double *conf;         /* [T]   confidence(metric) */
+  double *counts;       /* [N]   vote tally the policy used */
+  uint8_t *retained;    /* [N]   1 = expert retained */
+  int32_t *assigned;    /* [T,k] remap_assigned */
+  double *weights;      /* [T,k] remap_weights (renormalised) */
+  uint8_t *important;   /* [T]   accuracy policy's important tokens */
+  int32_t *flags;       /* [1]   LYNX_FLAG_* */
+} lynx_selection_t;
+
+/* One MoE layer's static description (weights are borrowed device memory). */
+typedef struct lynx_layer {
+  int32_t num_experts;    /* N */
+  int32_t top_k;          /* k */
+  int32_t d_model;        /* d, multiple of 8 */
+  int32_t d_ff;           /* ff, multiple of 8 */
+  int32_t activation;     /* lynx_activation */
+  int32_t reserved;
+  /* SWIGLU: packed gate/up [N, 2*ceil64(ff), d] (lynx_pack_w13 layout).
+   * TANH2:  w1^T [N, ff, d] (reference w1 is [N, d, ff], simulator.py:40). */
+  const uint16_t *w13;
+  const uint16_t *w2;        /* [N, d, ff]  (reference w2 [N, ff, d] transposed) */
+  const uint16_t *router_wt; /* [N, d]      (reference router_w [d, N] transposed); may be NULL
+                                if the caller routes itself */
+} lynx_layer_t;
+
+/* Dispatch produced by lynx_permute (simulator.py:104-112 order: experts
+ * ascending, token rows ascending, duplicate slots of a token merged). */
+typedef struct lynx_dispatch {
+  int32_t *n_seg;       /* [1]  number of segments (used experts split at LYNX_SEG_ROWS) */
+  int32_t *n_used;      /* [1]  number of used experts */
+  int32_t *seg_expert;  /* [max_seg] expert id of each segment */
+  int32_t *seg_row;     /* [max_seg] first permuted row (16-aligned) */
+  int32_t *seg_count;   /* [max_seg] token rows in the segment */
+  int32_t *perm_token;  /* [rows_cap] source token of each permuted row, -1 = padding */
+  float *perm_weight;   /* [rows_cap] merged gate weight of each permuted row */
+  int32_t *tok_rows;    /* [T,k] permuted rows of token t, experts ascending, -1 padded */
+  float *tok_weight;    /* [T,k] matching merged weights */
+  uint16_t *x_perm;     /* [rows_cap, d] gathered hidden rows (bf16), padding rows zero */
+} lynx_dispatch_t;
+
+/* ---- sizes ---------------------------------------------------------- */
+int lynx_abi_version(void);
+const char *lynx_status_string(int status);
+/* Upper bounds the caller uses to size dispatch buffers. */
+int lynx_dispatch_caps(int T, int N, int k, int32_t *max_seg, int32_t *rows_cap);
+/* Workspace for lynx_moe_forward / lynx_moe_layer. */
+size_t lynx_moe_workspace_bytes(const lynx_layer_t *layer, int T);
+
+/* ---- K0: router GEMV with fused RMSNorm (simulator.py:26-27, 82-83) -- */
+int lynx_router_logits(const uint16_t *hidden, const uint16_t *router_wt, int T, int d, int N,
+                       double *logits, lynx_stream_t stream);
+
+/* ---- K1: route_batch + apply_policy (router.py:174-187, policy.py:341-350) */
+int lynx_route_select(const double *logits, int T, int N, int k, int decode,
+                      const lynx_policy_t *policy, const lynx_selection_t *out,
+                      lynx_stream_t stream);
+
+/* apply_policy / latency_policy / accuracy_policy / full_retain_mask on an
+ * existing selection (policy.py:215-350).  expert_ids/probs/full_probs are
+ * inputs ([T,k], [T,k], [T,N]); out->expert_ids/probs/full_probs are ignored.
+ * policy NULL or mode NONE = full_retain_mask (also fills conf). */
+int lynx_apply_policy(const int32_t *expert_ids, const double *probs, const double *full_probs,
+                      int T, int N, int k, int decode, const lynx_policy_t *policy,
+                      const lynx_selection_t *out, lynx_stream_t stream);
+
+/* top_k_select (router.py:157-171) on float64 rows [T,N]: (value desc, index asc). */
+int lynx_topk(const double *values, int T, int N, int k, int32_t *ids, double *out,
+              lynx_stream_t stream);
+
+/* vote_expert_frequencies (policy.py:116-138); policy may carry rank weights. */
+int lynx_vote(const int32_t *expert_ids, int T, int k, int N, const lynx_policy_t *rank_weights,
+              double *counts, lynx_stream_t stream);
+
+/* remap_tokens on an arbitrary retained mask (policy.py:151-212). */
+int lynx_remap(const int32_t *expert_ids, const double *full_probs, int T, int N, int k,
+               const uint8_t *retained, int32_t *assigned, double *weights, int32_t *flags,
+               lynx_stream_t stream);
+
+/* ---- K2: histogram + scan permutation and gather (simulator.py:104-112) */
+int lynx_permute(const int32_t *assigned, const double *weights, const uint16_t *hidden,
+                 int T, int N, int k, int d, const lynx_dispatch_t *out, lynx_stream_t stream);
+
+/* ---- K3+K4: grouped expert FFN over used experts + weighted combine ---
+ * forward_layer(hidden, model, layer, mask) for a given mask. */
+int lynx_moe_forward(const lynx_layer_t *layer, const uint16_t *hidden, int T,
+                     const int32_t *assigned, const double *weights, uint16_t *out,
+                     void *workspace, size_t workspace_bytes, lynx_stream_t stream);
+
+/* Same as lynx_moe_forward but writes the f32 sum of expert outputs WITHOUT
+ * the residual; assigned entries < 0 are skipped (expert-parallel partial). */
+int lynx_moe_forward_partial(const lynx_layer_t *layer, const uint16_t *hidden, int T,
+                             const int32_t *assigned, const double *weights, float *partial_out,
+                             void *workspace, size_t workspace_bytes, lynx_stream_t stream);
+
+/* ---- whole decode layer: K0 -> K1 -> K2 -> K3 -> K4 ------------------
+ * _apply_routing + forward_layer (simulator.py:245-266, 86-113).
+ * `sel` may be NULL; when given, the selection/mask outputs are copied out. */
+int lynx_moe_layer(const lynx_layer_t *layer, const uint16_t *hidden, int T, int decode,
+                   const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,
+                   void *workspace, size_t workspace_bytes, lynx_stream_t stream);
+
+/* Pack HF-layout gate/up projections w1, w3 [N, ff, d] into the
+ * interleaved w13 layout the SwiGLU kernel streams. */
+int lynx_pack_w13(const uint16_t *w1, const uint16_t *w3, int N, int ff, int d, uint16_t *w13,
+                  lynx_stream_t stream);
+
+/* ---- expert parallel helpers -------------------------
+ * Rank r of G owns experts [r*N/G, (r+1)*N/G).  Dispatch rows are sent with
+ * a fixed per-peer capacity of T_local rows so the NCCL all-to-all needs no
+ * count exchange; every rank holds the identical global selection. */
+int lynx_ep_pack(const uint16_t *hidden_local, const int32_t *assigned, int T_local, int k,
+                 int N, int G, int d, int rank, uint16_t *send, lynx_stream_t stream);
+int lynx_ep_local_mask(const int32_t *assigned, const double *weights, int T, int k, int N,
+                       int G, int rank, int32_t *assigned_local, double *weights_local,
+                       lynx_stream_t stream);
+int lynx_ep_combine(const uint16_t *hidden_local, const float *recv_partial, int T_local, int G,
+                    int d, uint16_t *out, lynx_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LYNX_B200_H */

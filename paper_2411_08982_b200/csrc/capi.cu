@@ -1,0 +1,571 @@
+// capi.cu -- extern "C" entry points of include/lynx_b200.h: argument
+// validation mirroring the reference's ValidationError sites, workspace
+// planning, TMA descriptor encoding and the K0..K4 launch sequence.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "lynx_internal.cuh"
+
+using namespace lynx;
+
+namespace {
+
+constexpr int kAbiVersion = 1;
+
+int sm_count_cached() {
+  static int cached_dev = -1, cached = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev != cached_dev) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    cached = n;
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 tensor, dim0 contiguous, 128B swizzle, OOB -> zero.
+bool encode_bf16(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint32_t* box) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[3], gstride[2];
+  cuuint32_t bdim[3], estride[3] = {1, 1, 1};
+  uint64_t stride = 2;
+  for (int i = 0; i < rank; ++i) {
+    gdim[i] = dims[i];
+    bdim[i] = box[i];
+    if (i > 0) gstride[i - 1] = stride;
+    stride *= dims[i];
+  }
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), gdim, gstride, bdim, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int kb2_per_unit() {
+  static int v = 0;
+  if (!v) {
+    const char* s = getenv("LYNX_KB2_PER");
+    v = s ? atoi(s) : 32;
+    if (v < 1) v = 32;
+  }
+  return v;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Caps {
+  int max_seg, rows_cap;
+};
+
+Caps caps_for(int T, int N, int k) {
+  const int slots = T * k;
+  Caps c;
+  c.max_seg = std::min(N, slots) + slots / LYNX_SEG_ROWS + 1;
+  c.rows_cap = static_cast<int>(align_up(static_cast<size_t>(slots) + 15 * std::min(N, slots), 16));
+  return c;
+}
+
+struct Geometry {
+  int rows1, tiles1, kb1, tiles2, kb2_total, kb2_per, split2, bn;
+};
+
+Geometry geometry(const lynx_layer_t* L, int T) {
+  Geometry g;
+  g.rows1 = L->activation == LYNX_ACT_SWIGLU ? swiglu_rows(L->d_ff) : L->d_ff;
+  g.tiles1 = (g.rows1 + 127) / 128;
+  g.kb1 = (L->d_model + 63) / 64;
+  g.tiles2 = (L->d_model + 127) / 128;
+  g.kb2_total = (L->d_ff + 63) / 64;
+  g.kb2_per = std::min(g.kb2_total, kb2_per_unit());
+  g.split2 = (g.kb2_total + g.kb2_per - 1) / g.kb2_per;
+  const int rows = std::min(T, LYNX_SEG_ROWS);
+  g.bn = rows <= 32 ? 32 : rows <= 64 ? 64 : rows <= 128 ? 128 : 256;
+  return g;
+}
+
+// Workspace carve-up.  Selection region only for the whole-layer call.
+struct Plan {
+  size_t logits, ids, probs, full, conf, counts, retained, assigned, weights, important, flags;
+  size_t n_seg, n_used, seg_expert, seg_row, seg_count, perm_token, perm_weight, tok_rows, tok_weight;
+  size_t counters, x_perm, h, partial;
+  size_t total;
+  int n_counters;
+};
+
+Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
+  const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
+  const Caps c = caps_for(T, N, k);
+  const Geometry g = geometry(L, T);
+  Plan p{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  if (selection) {
+    p.logits = take(sizeof(double) * T * N);
+    p.ids = take(sizeof(int32_t) * T * k);
+    p.probs = take(sizeof(double) * T * k);
+    p.full = take(sizeof(double) * T * N);
+    p.conf = take(sizeof(double) * T);
+    p.counts = take(sizeof(double) * N);
+    p.retained = take(N);
+    p.assigned = take(sizeof(int32_t) * T * k);
+    p.weights = take(sizeof(double) * T * k);
+    p.important = take(T);
+    p.flags = take(sizeof(int32_t));
+  }
+  p.n_seg = take(sizeof(int32_t));
+  p.n_used = take(sizeof(int32_t));
+  p.seg_expert = take(sizeof(int32_t) * c.max_seg);
+  p.seg_row = take(sizeof(int32_t) * c.max_seg);
+  p.seg_count = take(sizeof(int32_t) * c.max_seg);
+  p.perm_token = take(sizeof(int32_t) * c.rows_cap);
+  p.perm_weight = take(sizeof(float) * c.rows_cap);
+  p.tok_rows = take(sizeof(int32_t) * T * k);
+  p.tok_weight = take(sizeof(float) * T * k);
+  p.n_counters = 1 + c.max_seg;
+  p.counters = take(sizeof(int32_t) * p.n_counters);
+  p.x_perm = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * d);
+  p.h = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * ff);
+  p.partial = take(sizeof(float) * static_cast<size_t>(g.split2) * c.rows_cap * d);
+  p.total = off + 256;  // slack for base alignment
+  return p;
+}
+
+template <typename T>
+T* at(void* base, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+int check_layer(const lynx_layer_t* L, int T) {
+  if (!L) return LYNX_ERR_SHAPE;
+  if (T < 1 || L->num_experts < 1 || L->d_model < 8 || L->d_ff < 8) return LYNX_ERR_SHAPE;
+  if (L->top_k < 1 || L->top_k > L->num_experts) return LYNX_ERR_TOPK;
+  if (L->num_experts > LYNX_MAX_EXPERTS || L->top_k > LYNX_MAX_TOPK || T > LYNX_MAX_TOKENS)
+    return LYNX_ERR_UNSUPPORTED;
+  if (L->d_model % 8 || L->d_ff % 8) return LYNX_ERR_UNSUPPORTED;  // TMA 16-byte strides
+  if (L->activation != LYNX_ACT_SWIGLU && L->activation != LYNX_ACT_TANH2) return LYNX_ERR_CONFIG;
+  if (!L->w13 || !L->w2) return LYNX_ERR_SHAPE;
+  return LYNX_OK;
+}
+
+// PolicyConfig.__post_init__ (policy.py:40-55) + the checks the reference
+// performs lazily on the decode path (policy.py:61-64, 130-133).
+int check_policy(const lynx_policy_t* pol, int N, int k, int decode, int* floor_keep) {
+  *floor_keep = k;
+  if (!pol || pol->mode == LYNX_POLICY_NONE) return LYNX_OK;
+  if (pol->mode != LYNX_POLICY_LATENCY && pol->mode != LYNX_POLICY_ACCURACY) return LYNX_ERR_CONFIG;
+  if (pol->drop_count < 0 || !(pol->confidence_threshold >= 0.0 && pol->confidence_threshold <= 1.0) ||
+      pol->sample_threshold < 1 || pol->min_experts < 0 || pol->freq_keep_budget < 1 ||
+      (pol->confidence_metric != LYNX_CONF_TOP1 && pol->confidence_metric != LYNX_CONF_MARGIN) ||
+      pol->n_rank_weights < 0 || pol->n_rank_weights > LYNX_MAX_TOPK)
+    return LYNX_ERR_CONFIG;
+  for (int r = 0; r < pol->n_rank_weights; ++r)
+    if (!(pol->rank_weights[r] >= 0.0)) return LYNX_ERR_CONFIG;
+  if (!decode) return LYNX_OK;
+  if (pol->min_experts > 0 && pol->min_experts < k) return LYNX_ERR_MIN_EXPERTS;
+  if (pol->n_rank_weights != 0 && pol->n_rank_weights != k) return LYNX_ERR_CONFIG;
+  if (pol->min_experts > 0) *floor_keep = pol->min_experts;
+  (void)N;
+  return LYNX_OK;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? LYNX_OK : LYNX_ERR_CUDA; }
+
+// K2 -> K3 -> K4 for a given mask (assigned/weights in device memory).
+int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int32_t* assigned,
+                 const double* weights, uint16_t* out_bf16, float* out_f32, void* ws, const Plan& P,
+                 cudaStream_t s) {
+  const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return LYNX_ERR_CUDA;
+  const Caps c = caps_for(T, N, k);
+  const Geometry g = geometry(L, T);
+
+  DispatchView dv;
+  dv.n_seg = at<int32_t>(ws, P.n_seg);
+  dv.n_used = at<int32_t>(ws, P.n_used);
+  dv.seg_expert = at<int32_t>(ws, P.seg_expert);
+  dv.seg_row = at<int32_t>(ws, P.seg_row);
+  dv.seg_count = at<int32_t>(ws, P.seg_count);
+  dv.perm_token = at<int32_t>(ws, P.perm_token);
+  dv.perm_weight = at<float>(ws, P.perm_weight);
+  dv.tok_rows = at<int32_t>(ws, P.tok_rows);
+  dv.tok_weight = at<float>(ws, P.tok_weight);
+  dv.x_perm = at<uint16_t>(ws, P.x_perm);
+  int* counters = at<int>(ws, P.counters);
+
+  PermuteArgs pa;
+  pa.assigned = assigned;
+  pa.weights = weights;
+  pa.hidden = hidden;
+  pa.T = T;
+  pa.N = N;
+  pa.k = k;
+  pa.d = d;
+  pa.max_seg = c.max_seg;
+  pa.rows_cap = c.rows_cap;
+  pa.out = dv;
+  pa.counters = counters;
+  pa.n_counters = P.n_counters;
+  int st = cuda_status(launch_permute(pa, sms, s));
+  if (st) return st;
+
+  FfnParams fp;
+  {
+    const uint64_t dw1[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(g.rows1), static_cast<uint64_t>(N)};
+    const uint64_t dw2[3] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(d), static_cast<uint64_t>(N)};
+    const uint64_t dx[2] = {static_cast<uint64_t>(d), static_cast<uint64_t>(c.rows_cap)};
+    const uint64_t dh[2] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(c.rows_cap)};
+    const uint32_t bw[3] = {64, 128, 1};
+    const uint32_t ba[2] = {64, 16};
+    if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw) ||
+        !encode_bf16(&fp.map_x, dv.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
+      return LYNX_ERR_CUDA;
+  }
+  fp.n_seg = dv.n_seg;
+  fp.seg_expert = dv.seg_expert;
+  fp.seg_row = dv.seg_row;
+  fp.seg_count = dv.seg_count;
+  fp.h = at<uint16_t>(ws, P.h);
+  fp.partial = at<float>(ws, P.partial);
+  fp.counters = counters;
+  fp.d = d;
+  fp.ff = ff;
+  fp.act = L->activation;
+  fp.tiles1 = g.tiles1;
+  fp.kb1 = g.kb1;
+  fp.tiles2 = g.tiles2;
+  fp.split2 = g.split2;
+  fp.kb2_per = g.kb2_per;
+  fp.kb2_total = g.kb2_total;
+  fp.rows_cap = c.rows_cap;
+  st = cuda_status(launch_ffn(fp, g.bn, sms, s));
+  if (st) return st;
+
+  CombineArgs ca;
+  ca.hidden = out_f32 ? nullptr : hidden;
+  ca.partial = fp.partial;
+  ca.split2 = g.split2;
+  ca.rows_cap = c.rows_cap;
+  ca.T = T;
+  ca.k = k;
+  ca.d = d;
+  ca.tok_rows = dv.tok_rows;
+  ca.tok_weight = dv.tok_weight;
+  ca.out_bf16 = out_bf16;
+  ca.out_f32 = out_f32;
+  return cuda_status(launch_combine(ca, s));
+}
+
+void* aligned_ws(void* ws) {
+  return reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+}
+
+}  // namespace
+
+extern "C" {
+
+int lynx_abi_version(void) { return kAbiVersion; }
+
+const char* lynx_status_string(int status) {
+  switch (status) {
+    case LYNX_OK:
+      return "ok";
+    case LYNX_ERR_SHAPE:
+      return "invalid shape";
+    case LYNX_ERR_TOPK:
+      return "k out of range";
+    case LYNX_ERR_MIN_EXPERTS:
+      return "min_experts must be >= top_k";
+    case LYNX_ERR_RETAINED:
+      return "retained set empty or out of range";
+    case LYNX_ERR_TOKENS:
+      return "token count mismatch";
+    case LYNX_ERR_CUDA:
+      return "CUDA error";
+    case LYNX_ERR_UNSUPPORTED:
+      return "shape outside build limits";
+    case LYNX_ERR_WORKSPACE:
+      return "workspace too small";
+    case LYNX_ERR_CONFIG:
+      return "invalid policy config";
+    default:
+      return "unknown status";
+  }
+}
+
+int lynx_dispatch_caps(int T, int N, int k, int32_t* max_seg, int32_t* rows_cap) {
+  if (T < 1 || N < 1 || k < 1) return LYNX_ERR_SHAPE;
+  const Caps c = caps_for(T, N, k);
+  if (max_seg) *max_seg = c.max_seg;
+  if (rows_cap) *rows_cap = c.rows_cap;
+  return LYNX_OK;
+}
+
+size_t lynx_moe_workspace_bytes(const lynx_layer_t* layer, int T) {
+  if (!layer || T < 1) return 0;
+  return plan_for(layer, T, true).total;
+}
+
+int lynx_router_logits(const uint16_t* hidden, const uint16_t* router_wt, int T, int d, int N, double* logits,
+                       lynx_stream_t stream) {
+  if (T < 1 || N < 1 || d < 8) return LYNX_ERR_SHAPE;
+  if (d % 8 || N > LYNX_MAX_EXPERTS) return LYNX_ERR_UNSUPPORTED;
+  return cuda_status(launch_router_logits(hidden, router_wt, T, d, N, logits, stream));
+}
+
+int lynx_route_select(const double* logits, int T, int N, int k, int decode, const lynx_policy_t* policy,
+                      const lynx_selection_t* out, lynx_stream_t stream) {
+  if (T < 1 || N < 1) return LYNX_ERR_SHAPE;
+  if (k < 1 || k > N) return LYNX_ERR_TOPK;
+  if (N > LYNX_MAX_EXPERTS || k > LYNX_MAX_TOPK || T > LYNX_MAX_TOKENS) return LYNX_ERR_UNSUPPORTED;
+  if (!out || !out->expert_ids || !out->probs || !out->full_probs || !out->conf || !out->assigned ||
+      !out->weights || !out->flags)
+    return LYNX_ERR_SHAPE;
+  int floor_keep = k;
+  const int st = check_policy(policy, N, k, decode, &floor_keep);
+  if (st) return st;
+  SelectArgs a;
+  a.logits = logits;
+  a.T = T;
+  a.N = N;
+  a.k = k;
+  a.decode = decode;
+  if (policy) {
+    a.pol = *policy;
+  } else {
+    a.pol = lynx_policy_t{};
+    a.pol.mode = LYNX_POLICY_NONE;
+  }
+  a.floor_keep = floor_keep;
+  a.ids = out->expert_ids;
+  a.probs = out->probs;
+  a.full = out->full_probs;
+  a.conf = out->conf;
+  a.counts = out->counts;
+  a.retained = out->retained;
+  a.assigned = out->assigned;
+  a.weights = out->weights;
+  a.important = out->important;
+  a.flags = out->flags;
+  return cuda_status(launch_route_select(a, stream));
+}
+
+int lynx_apply_policy(const int32_t* expert_ids, const double* probs, const double* full_probs, int T, int N, int k,
+                      int decode, const lynx_policy_t* policy, const lynx_selection_t* out, lynx_stream_t stream) {
+  if (T < 1 || N < 1) return LYNX_ERR_SHAPE;
+  if (k < 1 || k > N) return LYNX_ERR_TOPK;
+  if (N > LYNX_MAX_EXPERTS || k > LYNX_MAX_TOPK || T > LYNX_MAX_TOKENS) return LYNX_ERR_UNSUPPORTED;
+  if (!out || !expert_ids || !probs || !full_probs || !out->conf || !out->assigned || !out->weights || !out->flags)
+    return LYNX_ERR_SHAPE;
+  int floor_keep = k;
+  const int st = check_policy(policy, N, k, decode, &floor_keep);
+  if (st) return st;
+  SelectArgs a;
+  a.logits = nullptr;
+  a.T = T;
+  a.N = N;
+  a.k = k;
+  a.decode = decode;
+  if (policy) {
+    a.pol = *policy;
+  } else {
+    a.pol = lynx_policy_t{};
+    a.pol.mode = LYNX_POLICY_NONE;
+  }
+  a.floor_keep = floor_keep;
+  a.ids = const_cast<int32_t*>(expert_ids);
+  a.probs = const_cast<double*>(probs);
+  a.full = const_cast<double*>(full_probs);
+  a.conf = out->conf;
+  a.counts = out->counts;
+  a.retained = out->retained;
+  a.assigned = out->assigned;
+  a.weights = out->weights;
+  a.important = out->important;
+  a.flags = out->flags;
+  return cuda_status(launch_route_select(a, stream));
+}
+
+int lynx_topk(const double* values, int T, int N, int k, int32_t* ids, double* out, lynx_stream_t stream) {
+  if (T < 1 || N < 1) return LYNX_ERR_SHAPE;
+  if (k < 1 || k > N) return LYNX_ERR_TOPK;
+  if (N > LYNX_MAX_EXPERTS) return LYNX_ERR_UNSUPPORTED;
+  return cuda_status(launch_topk(values, T, N, k, ids, out, stream));
+}
+
+int lynx_vote(const int32_t* expert_ids, int T, int k, int N, const lynx_policy_t* rank_weights, double* counts,
+              lynx_stream_t stream) {
+  if (T < 1 || N < 1 || k < 1) return LYNX_ERR_SHAPE;
+  if (N > LYNX_MAX_EXPERTS || k > LYNX_MAX_TOPK) return LYNX_ERR_UNSUPPORTED;
+  lynx_policy_t w{};
+  if (rank_weights && rank_weights->n_rank_weights) {
+    if (rank_weights->n_rank_weights != k) return LYNX_ERR_CONFIG;
+    w = *rank_weights;
+  }
+  return cuda_status(launch_vote(expert_ids, T, k, N, w, counts, stream));
+}
+
+int lynx_remap(const int32_t* expert_ids, const double* full_probs, int T, int N, int k, const uint8_t* retained,
+               int32_t* assigned, double* weights, int32_t* flags, lynx_stream_t stream) {
+  if (T < 1 || N < 1) return LYNX_ERR_SHAPE;
+  if (k < 1 || k > N) return LYNX_ERR_TOPK;
+  if (N > LYNX_MAX_EXPERTS || k > LYNX_MAX_TOPK) return LYNX_ERR_UNSUPPORTED;
+  if (!retained) return LYNX_ERR_RETAINED;
+  return cuda_status(launch_remap(expert_ids, full_probs, T, N, k, retained, assigned, weights, flags, stream));
+}
+
+int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t* hidden, int T, int N, int k, int d,
+                 const lynx_dispatch_t* out, lynx_stream_t stream) {
+  if (T < 1 || N < 1 || d < 8) return LYNX_ERR_SHAPE;
+  if (k < 1 || k > N) return LYNX_ERR_TOPK;
+  if (N > LYNX_MAX_EXPERTS || k > LYNX_MAX_TOPK || T > LYNX_MAX_TOKENS || d % 8) return LYNX_ERR_UNSUPPORTED;
+  if (!out) return LYNX_ERR_SHAPE;
+  const int sms = sm_count_cached();
+  if (sms <= 0) return LYNX_ERR_CUDA;
+  const Caps c = caps_for(T, N, k);
+  PermuteArgs pa;
+  pa.assigned = assigned;
+  pa.weights = weights;
+  pa.hidden = hidden;
+  pa.T = T;
+  pa.N = N;
+  pa.k = k;
+  pa.d = d;
+  pa.max_seg = c.max_seg;
+  pa.rows_cap = c.rows_cap;
+  pa.out.n_seg = out->n_seg;
+  pa.out.n_used = out->n_used;
+  pa.out.seg_expert = out->seg_expert;
+  pa.out.seg_row = out->seg_row;
+  pa.out.seg_count = out->seg_count;
+  pa.out.perm_token = out->perm_token;
+  pa.out.perm_weight = out->perm_weight;
+  pa.out.tok_rows = out->tok_rows;
+  pa.out.tok_weight = out->tok_weight;
+  pa.out.x_perm = out->x_perm;
+  pa.counters = nullptr;
+  pa.n_counters = 0;
+  return cuda_status(launch_permute(pa, sms, stream));
+}
+
+static int moe_forward_common(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
+                              const double* weights, uint16_t* out_bf16, float* out_f32, void* workspace,
+                              size_t workspace_bytes, lynx_stream_t stream) {
+  int st = check_layer(layer, T);
+  if (st) return st;
+  const Plan P = plan_for(layer, T, false);
+  if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
+  return forward_impl(layer, hidden, T, assigned, weights, out_bf16, out_f32, aligned_ws(workspace), P, stream);
+}
+
+int lynx_moe_forward(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
+                     const double* weights, uint16_t* out, void* workspace, size_t workspace_bytes,
+                     lynx_stream_t stream) {
+  return moe_forward_common(layer, hidden, T, assigned, weights, out, nullptr, workspace, workspace_bytes, stream);
+}
+
+/* Same as lynx_moe_forward, but writes the f32 expert sum WITHOUT the
+ * residual (expert-parallel partial; assigned entries < 0 are skipped). */
+int lynx_moe_forward_partial(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
+                             const double* weights, float* partial_out, void* workspace, size_t workspace_bytes,
+                             lynx_stream_t stream) {
+  return moe_forward_common(layer, hidden, T, assigned, weights, nullptr, partial_out, workspace, workspace_bytes,
+                            stream);
+}
+
+int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
+                   uint16_t* out, const lynx_selection_t* sel, void* workspace, size_t workspace_bytes,
+                   lynx_stream_t stream) {
+  int st = check_layer(layer, T);
+  if (st) return st;
+  if (!layer->router_wt) return LYNX_ERR_SHAPE;
+  const int N = layer->num_experts, k = layer->top_k;
+  int floor_keep = k;
+  st = check_policy(policy, N, k, decode, &floor_keep);
+  if (st) return st;
+  const Plan P = plan_for(layer, T, true);
+  if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
+  void* ws = aligned_ws(workspace);
+
+  double* logits = at<double>(ws, P.logits);
+  st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, logits, stream));
+  if (st) return st;
+
+  SelectArgs a;
+  a.logits = logits;
+  a.T = T;
+  a.N = N;
+  a.k = k;
+  a.decode = decode;
+  if (policy) {
+    a.pol = *policy;
+  } else {
+    a.pol = lynx_policy_t{};
+    a.pol.mode = LYNX_POLICY_NONE;
+  }
+  a.floor_keep = floor_keep;
+#define LYNX_PICK(field, off, type) ((sel && sel->field) ? sel->field : at<type>(ws, P.off))
+  a.ids = LYNX_PICK(expert_ids, ids, int32_t);
+  a.probs = LYNX_PICK(probs, probs, double);
+  a.full = LYNX_PICK(full_probs, full, double);
+  a.conf = LYNX_PICK(conf, conf, double);
+  a.counts = LYNX_PICK(counts, counts, double);
+  a.retained = LYNX_PICK(retained, retained, uint8_t);
+  a.assigned = LYNX_PICK(assigned, assigned, int32_t);
+  a.weights = LYNX_PICK(weights, weights, double);
+  a.important = LYNX_PICK(important, important, uint8_t);
+  a.flags = LYNX_PICK(flags, flags, int32_t);
+#undef LYNX_PICK
+  st = cuda_status(launch_route_select(a, stream));
+  if (st) return st;
+  return forward_impl(layer, hidden, T, a.assigned, a.weights, out, nullptr, ws, P, stream);
+}
+
+int lynx_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,
+                  lynx_stream_t stream) {
+  if (N < 1 || ff < 1 || d < 1) return LYNX_ERR_SHAPE;
+  return cuda_status(launch_pack_w13(w1, w3, N, ff, d, w13, stream));
+}
+
+int lynx_ep_pack(const uint16_t* hidden_local, const int32_t* assigned, int T_local, int k, int N, int G, int d,
+                 int rank, uint16_t* send, lynx_stream_t stream) {
+  if (T_local < 1 || G < 1 || N % G || rank < 0 || rank >= G || d % 8) return LYNX_ERR_SHAPE;
+  return cuda_status(launch_ep_pack(hidden_local, assigned, T_local, k, N, G, d, rank, send, stream));
+}
+
+int lynx_ep_local_mask(const int32_t* assigned, const double* weights, int T, int k, int N, int G, int rank,
+                       int32_t* assigned_local, double* weights_local, lynx_stream_t stream) {
+  if (T < 1 || G < 1 || N % G || rank < 0 || rank >= G) return LYNX_ERR_SHAPE;
+  return cuda_status(launch_ep_local_mask(assigned, weights, T, k, N, G, rank, assigned_local, weights_local, stream));
+}
+
+int lynx_ep_combine(const uint16_t* hidden_local, const float* recv_partial, int T_local, int G, int d,
+                    uint16_t* out, lynx_stream_t stream) {
+  if (T_local < 1 || G < 1 || d % 2) return LYNX_ERR_SHAPE;
+  return cuda_status(launch_ep_combine(hidden_local, recv_partial, T_local, G, d, out, stream));
+}
+
+}  // extern "C"

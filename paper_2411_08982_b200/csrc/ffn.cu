@@ -1,0 +1,329 @@
+// ffn.cu -- K3: grouped expert FFN over the USED experts only, on the
+// 5th-gen tensor cores (tcgen05.mma, accumulators in TMEM), operands staged
+// by TMA into 128B-swizzled shared memory.
+//
+// Reference: forward_layer (simulator.py:86-113) calls expert_mlp
+// (simulator.py:77-79) once per used expert on that expert's token rows.
+// Here every used expert becomes a "segment" of <= 256 token rows (built by
+// K2), and the whole layer's expert work is one persistent launch:
+//
+//   phase-0 unit (seg, mt):       D[128 x n] = W1[e][mt*128 : +128, :] . X_seg^T
+//        SwiGLU: rows interleave gate/up in 16-row groups (lynx_pack_w13),
+//        epilogue h = silu(gate) * up -> H[seg rows, 64 features] (bf16).
+//        TANH2:  epilogue h = tanh(acc) -> H[seg rows, 128 features].
+//   phase-1 unit (seg, mt, s):    D[128 x n] = W2[e][mt*128 : +128, K_s] . H_seg[:, K_s]^T
+//        epilogue -> partial[s][seg rows][mt*128 : +128] (f32), summed in a
+//        fixed order by K4 (deterministic, no float atomics).
+//
+// Swap-AB: weight rows are the MMA M (=128) dimension, the segment's tokens
+// the MMA N dimension (16..256, rounded to 16), so decode streams each used
+// expert's weights from HBM exactly once while the tiny activation tiles
+// come from L2.  Units are dequeued from a device ticket counter in order
+// [all phase-0 units][all phase-1 units]; a phase-1 unit waits (acquire)
+// until its segment's phase-0 tiles are published (release), which by
+// queue order has almost always already happened.
+//
+// Warp roles (256 threads, one CTA per SM):
+//   warp 0      TMA producer + unit scheduler (one elected lane)
+//   warp 1      tcgen05.mma issuer (one lane)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: TMEM -> registers -> activation -> global
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "lynx_internal.cuh"
+#include "ptx.cuh"
+
+namespace lynx {
+
+constexpr int kFfnThreads = 256;
+constexpr int kUnitRing = 4;
+constexpr int kTileA = 128 * 64 * 2;  // 128 weight rows x 64 bf16 (one 128B-swizzled k block)
+constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
+
+struct Unit {
+  int phase, seg, mt, split, kb0, kb1, expert, row0, n, nmma;
+};
+
+__device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u, Unit& U) {
+  if (u < 0) return false;
+  const int nA = nseg * p.tiles1;
+  if (u < nA) {
+    U.phase = 0;
+    U.seg = u / p.tiles1;
+    U.mt = u - U.seg * p.tiles1;
+    U.split = 0;
+    U.kb0 = 0;
+    U.kb1 = p.kb1;
+  } else {
+    const int v = u - nA;
+    const int per = p.tiles2 * p.split2;
+    U.phase = 1;
+    U.seg = v / per;
+    const int r = v - U.seg * per;
+    U.mt = r / p.split2;
+    U.split = r - U.mt * p.split2;
+    U.kb0 = U.split * p.kb2_per;
+    U.kb1 = min(p.kb2_total, U.kb0 + p.kb2_per);
+  }
+  U.expert = p.seg_expert[U.seg];
+  U.row0 = p.seg_row[U.seg];
+  U.n = p.seg_count[U.seg];
+  U.nmma = (U.n + 15) & ~15;
+  return true;
+}
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.f + __expf(-g)) * u; }
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_constant__ FfnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kTileB = BN * 128;
+  constexpr uint32_t kTmemCols = 2 * BN;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kTileA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kTileB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ufull = tempty + 2;
+  uint64_t* uempty = ufull + kUnitRing;
+  int* uring = reinterpret_cast<int*>(uempty + kUnitRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    for (int i = 0; i < kUnitRing; ++i) {
+      mbar_init(&ufull[i], 1);
+      mbar_init(&uempty[i], 5);  // MMA lane + 4 epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (threadIdx.x == 32) {
+    tma_prefetch_desc(&p.map_w1);
+    tma_prefetch_desc(&p.map_w2);
+    tma_prefetch_desc(&p.map_x);
+    tma_prefetch_desc(&p.map_h);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nseg = *p.n_seg;
+  const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_act = policy_evict_last();
+      int stage = 0, slot = 0;
+      uint32_t phase = 0, uphase = 0;
+      while (true) {
+        int u = atomicAdd(&p.counters[0], 1);
+        if (u >= total) u = -1;
+        mbar_wait(&uempty[slot], uphase ^ 1, 1);
+        uring[slot] = u;
+        mbar_arrive(&ufull[slot]);
+        if (++slot == kUnitRing) {
+          slot = 0;
+          uphase ^= 1;
+        }
+        Unit U;
+        if (!decode_unit(p, nseg, u, U)) break;
+        const CUtensorMap* ma = U.phase == 0 ? &p.map_w1 : &p.map_w2;
+        const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
+        if (U.phase == 1) {
+          const int* done = p.counters + 1 + U.seg;
+          Watchdog wd;
+          while (ld_acquire_gpu(done) < 4 * p.tiles1) {
+            __nanosleep(100);
+            wd.tick(2);
+          }
+          fence_proxy_async();  // H was written by generic stores; TMA reads it
+        }
+        const int nb = U.nmma >> 4;
+        const uint32_t bytes = kTileA + nb * kBoxB;
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1, 3);
+          mbar_expect_tx(&full[stage], bytes);
+          tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, uphase = 0, aphase = 0;
+      while (true) {
+        mbar_wait(&ufull[slot], uphase, 4);
+        const int u = uring[slot];
+        mbar_arrive(&uempty[slot]);
+        if (++slot == kUnitRing) {
+          slot = 0;
+          uphase ^= 1;
+        }
+        Unit U;
+        if (!decode_unit(p, nseg, u, U)) break;
+        const uint32_t idesc = idesc_bf16_f32(128, U.nmma);
+        mbar_wait(&tempty[acc], aphase ^ 1, 5);
+        tc_fence_after();
+        const uint32_t dt = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+          mbar_wait(&full[stage], phase, 6);
+          tc_fence_after();
+          const uint64_t ad = sdesc_kmajor_sw128(smem_u32(sA + stage * kTileA));
+          const uint64_t bd = sdesc_kmajor_sw128(smem_u32(sB + stage * kTileB));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide block; +32 B = +2 in the address field
+            umma_bf16_ss(dt, ad + 2 * k, bd + 2 * k, idesc, (kb > U.kb0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------- epilogue
+    const int q = warp - 4;  // TMEM lane quarter (warp_id % 4)
+    int slot = 0, acc = 0;
+    uint32_t uphase = 0, aphase = 0;
+    while (true) {
+      mbar_wait(&ufull[slot], uphase, 7);
+      const int u = uring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&uempty[slot]);
+      if (++slot == kUnitRing) {
+        slot = 0;
+        uphase ^= 1;
+      }
+      Unit U;
+      if (!decode_unit(p, nseg, u, U)) break;
+      mbar_wait(&tfull[acc], aphase, 8);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      if (U.phase == 0) {
+        __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(p.h);
+        if (p.act == LYNX_ACT_SWIGLU) {
+          // lanes 0-15: gate rows, lanes 16-31: up rows of the same 16 features
+          const int f = U.mt * 64 + q * 16 + (lane & 15);
+          const bool upper = lane >= 16;
+          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tb + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float send = __uint_as_float(upper ? v[j] : v[8 + j]);
+              const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+              const float g = upper ? recv : __uint_as_float(v[j]);
+              const float uu = upper ? __uint_as_float(v[8 + j]) : recv;
+              const int tok = c0 + (upper ? 8 : 0) + j;
+              if (tok < U.n && f < p.ff)
+                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(silu_mul(g, uu));
+            }
+          }
+        } else {
+          const int f = U.mt * 128 + q * 32 + lane;
+          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tb + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int tok = c0 + j;
+              if (tok < U.n && f < p.ff)
+                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(tanhf(__uint_as_float(v[j])));
+            }
+          }
+        }
+      } else {
+        const int r = U.mt * 128 + q * 32 + lane;
+        float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
+        for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tb + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int tok = c0 + j;
+            if (tok < U.n && r < p.d) dst[static_cast<size_t>(tok) * p.d] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (U.phase == 0) {
+        // publish this warp's slice of H to phase-1 consumers on other SMs
+        __threadfence();
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
+      }
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s) {
+  constexpr size_t smem =
+      1024 + STAGES * (kTileA + BN * 128) + (2 * STAGES + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
+  static int configured_device = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_device != dev) {
+    cudaError_t e = cudaFuncSetAttribute(ffn_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured_device = dev;
+  }
+  ffn_kernel<BN, STAGES><<<sm_count, kFfnThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s) {
+  switch (bn) {
+    case 32:
+      return launch_ffn_t<32, 10>(p, sm_count, s);
+    case 64:
+      return launch_ffn_t<64, 8>(p, sm_count, s);
+    case 128:
+      return launch_ffn_t<128, 6>(p, sm_count, s);
+    default:
+      return launch_ffn_t<256, 4>(p, sm_count, s);
+  }
+}
+
+}  // namespace lynx

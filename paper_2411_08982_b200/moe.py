@@ -1,0 +1,308 @@
+"""MoE decode layer on the GPU -- mirror of the hot-path part of
+moetrim.simulator (simulator.py:26-113, 245-266).
+
+* ``MoEWeights``     -- the per-layer expert/router weights in the layouts the
+                        kernels stream (bf16, K-major), i.e. the ``model``
+                        argument of ``forward_layer``.
+* ``router_logits``  -- simulator.py:82-83 (K0: RMSNorm fused into the GEMV).
+* ``forward_layer``  -- simulator.py:86-113 (K2 permute -> K3 grouped expert
+                        GEMM on tcgen05 -> K4 combine), same signature.
+* ``LynxMoELayer``   -- the whole decode layer (_apply_routing + forward_layer,
+                        simulator.py:245-266 + 86-113) as one stream-ordered,
+                        graph-capturable C call (lynx_moe_layer).
+
+Expert activations: ``"swiglu"`` (Mixtral's expert, the north-star path) or
+``"tanh2"`` (the reference's own ``tanh(x @ w1) @ w2``, simulator.py:77-79).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ValidationError
+from .policy import ExpertMask, PolicyConfig
+from .router import MoEModelSpec, Phase, ctypes_ref
+
+
+def _torch():
+    import torch
+    return torch
+
+
+ACTIVATIONS = {"swiglu": nat.ACT_SWIGLU, "tanh2": nat.ACT_TANH2}
+
+
+def swiglu_rows(ff: int) -> int:
+    """Rows of the packed gate/up matrix per expert (2 * ceil64(ff))."""
+    return 2 * ((ff + 63) // 64) * 64
+
+
+def w13_row_of(f: int, up: bool) -> int:
+    """Packed row holding feature f of w1 (up=False) or w3 (up=True) -- lynx_pack_w13."""
+    return 128 * (f // 64) + 32 * ((f % 64) // 16) + (16 if up else 0) + f % 16
+
+
+def unpack_w13(w13, ff: int):
+    """Inverse of lynx_pack_w13: packed [N, rows, d] -> (w1, w3) each [N, ff, d]."""
+    torch = _torch()
+    f = torch.arange(ff)
+    gate = 128 * (f // 64) + 32 * ((f % 64) // 16) + f % 16
+    idx = gate.to(w13.device)
+    return w13[:, idx], w13[:, idx + 16]
+
+
+def pack_w13(w1, w3):
+    """HF gate/up projections [N, ff, d] (bf16, CUDA) -> packed w13 (lynx_pack_w13 kernel)."""
+    torch = _torch()
+    N, ff, d = w1.shape
+    w13 = torch.empty((N, swiglu_rows(ff), d), dtype=torch.bfloat16, device=w1.device)
+    nat.check(nat.lib().lynx_pack_w13(nat.ptr(w1.contiguous()), nat.ptr(w3.contiguous()), N, ff, d,
+                                      nat.ptr(w13), nat.stream_handle()), "pack_w13")
+    return w13
+
+
+@dataclass
+class MoEWeights:
+    """Device weights of an MoE stack, per layer (the ``model`` of forward_layer).
+
+    swiglu: w13[l] packed [N, 2*ceil64(ff), d], w2[l] [N, d, ff]
+    tanh2:  w13[l] = w1^T [N, ff, d], w2[l] = w2^T [N, d, ff]
+    router_wt[l] = router_w^T [N, d]; all bf16, contiguous, CUDA.
+    """
+
+    spec: MoEModelSpec
+    activation: str
+    w13: list
+    w2: list
+    router_wt: list
+    _native: dict = field(default_factory=dict, repr=False)
+
+    def native_layer(self, layer: int) -> nat.LynxLayer:
+        if layer not in self._native:
+            s = self.spec
+            L = nat.LynxLayer()
+            L.num_experts, L.top_k, L.d_model, L.d_ff = s.num_experts, s.top_k, s.d_model, s.d_ff
+            L.activation = ACTIVATIONS[self.activation]
+            L.w13 = nat.ptr(self.w13[layer])
+            L.w2 = nat.ptr(self.w2[layer])
+            L.router_wt = nat.ptr(self.router_wt[layer]) if self.router_wt[layer] is not None else 0
+            self._native[layer] = L
+        return self._native[layer]
+
+    def expert_bytes(self) -> int:
+        """Bytes streamed per used expert per layer (all three projections, bf16)."""
+        s = self.spec
+        return 3 * s.d_model * s.d_ff * 2 if self.activation == "swiglu" else 2 * s.d_model * s.d_ff * 2
+
+
+def build_swiglu_model(spec: MoEModelSpec, seed: int = 0, router_gain: float = 2.0,
+                       device: str = "cuda") -> MoEWeights:
+    """Random-init SwiGLU stack (SURVEY 8d recipe, after simulator.py:44-74):
+    router ~ N(0, (gain/sqrt(d))^2), W1, W3 ~ N(0, 1/d), W2 ~ N(0, 1/ff); bf16."""
+    torch = _torch()
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    N, d, ff = spec.num_experts, spec.d_model, spec.d_ff
+    w13s, w2s, routers = [], [], []
+    for _ in range(spec.num_layers):
+        w13 = torch.randn((N, swiglu_rows(ff), d), generator=g, device=device, dtype=torch.bfloat16)
+        w13.mul_(1.0 / np.sqrt(d))
+        if ff % 64:  # zero the padding features of the packed layout
+            f = torch.arange(ff, swiglu_rows(ff) // 2)
+            for up in (False, True):
+                rows = 128 * (f // 64) + 32 * ((f % 64) // 16) + (16 if up else 0) + f % 16
+                w13[:, rows.to(device)] = 0
+        w2 = torch.randn((N, d, ff), generator=g, device=device, dtype=torch.bfloat16)
+        w2.mul_(1.0 / np.sqrt(ff))
+        r = torch.randn((N, d), generator=g, device=device, dtype=torch.bfloat16)
+        r.mul_(router_gain / np.sqrt(d))
+        w13s.append(w13)
+        w2s.append(w2)
+        routers.append(r)
+    return MoEWeights(spec, "swiglu", w13s, w2s, routers)
+
+
+def from_hf_swiglu(spec: MoEModelSpec, w1: list, w3: list, w2: list, router: list) -> MoEWeights:
+    """Per-layer HF Mixtral tensors: w1/w3 [N, ff, d], w2 [N, d, ff], router [N, d]."""
+    torch = _torch()
+    cast = lambda t: t.to(device="cuda", dtype=torch.bfloat16).contiguous()  # noqa: E731
+    return MoEWeights(spec, "swiglu", [pack_w13(cast(a), cast(b)) for a, b in zip(w1, w3)],
+                      [cast(t) for t in w2], [cast(t) for t in router])
+
+
+def from_reference(model) -> MoEWeights:
+    """A moetrim.simulator.SyntheticMoE (simulator.py:30-41) as bf16 tanh2 weights.
+
+    Duck-typed: needs ``spec``, ``router_w [L,d,N]``, ``w1 [L,N,d,ff]``, ``w2 [L,N,ff,d]``.
+    """
+    torch = _torch()
+    s = model.spec
+    spec = MoEModelSpec(s.num_layers, s.num_experts, s.top_k, s.d_model, s.d_ff, s.bytes_per_param)
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(  # noqa: E731
+        "cuda").to(torch.bfloat16).contiguous()
+    w1t = [bf(np.transpose(model.w1[l], (0, 2, 1))) for l in range(s.num_layers)]
+    w2t = [bf(np.transpose(model.w2[l], (0, 2, 1))) for l in range(s.num_layers)]
+    rt = [bf(np.transpose(model.router_w[l])) for l in range(s.num_layers)]
+    return MoEWeights(spec, "tanh2", w1t, w2t, rt)
+
+
+# ----------------------------------------------------------------- workspace
+_WS: dict = {}
+
+
+def _workspace(layer: nat.LynxLayer, T: int):
+    torch = _torch()
+    nbytes = int(nat.lib().lynx_moe_workspace_bytes(ctypes_ref(layer), T))
+    key = (torch.cuda.current_device(), nbytes)
+    buf = _WS.get(key)
+    if buf is None:
+        buf = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+        _WS[key] = buf
+    return buf
+
+
+def _hidden_bf16(hidden, d: int):
+    torch = _torch()
+    if isinstance(hidden, torch.Tensor):
+        h = hidden.to(device="cuda", dtype=torch.bfloat16)
+    else:
+        h = torch.from_numpy(np.ascontiguousarray(np.asarray(hidden, dtype=np.float32))).to("cuda").to(
+            torch.bfloat16)
+    if h.ndim != 2 or h.shape[1] != d:
+        raise ValidationError(f"hidden must be [T, {d}], got {tuple(h.shape)}")
+    return h.contiguous()
+
+
+def router_logits(model: MoEWeights, layer: int, hidden):
+    """rms_norm(hidden) @ router_w (simulator.py:26-27, 82-83) -> float64 [T, N]."""
+    torch = _torch()
+    s = model.spec
+    h = _hidden_bf16(hidden, s.d_model)
+    out = torch.empty((h.shape[0], s.num_experts), dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().lynx_router_logits(nat.ptr(h), nat.ptr(model.router_wt[layer]), h.shape[0], s.d_model,
+                                           s.num_experts, nat.ptr(out), nat.stream_handle()), "router_logits")
+    return out
+
+
+def forward_layer(hidden, model: MoEWeights, layer_index: int, mask: ExpertMask):
+    """MoE sublayer: residual + weighted sum of the assigned experts (simulator.py:86-113).
+
+    Returns bf16 [T, d] on the GPU.  Only experts with at least one assigned
+    slot are read from HBM.
+    """
+    torch = _torch()
+    s = model.spec
+    h = _hidden_bf16(hidden, s.d_model)
+    if h.shape[0] != mask.num_tokens:
+        raise ValidationError(f"mask covers {mask.num_tokens} tokens but hidden has {h.shape[0]}")
+    T = int(h.shape[0])
+    layer = model.native_layer(layer_index)
+    assigned = mask.remap_assigned.to(device="cuda", dtype=torch.int32).contiguous()
+    weights = mask.remap_weights.to(device="cuda", dtype=torch.float64).contiguous()
+    ws = _workspace(layer, T)
+    out = torch.empty_like(h)
+    nat.check(nat.lib().lynx_moe_forward(ctypes_ref(layer), nat.ptr(h), T, nat.ptr(assigned), nat.ptr(weights),
+                                         nat.ptr(out), nat.ptr(ws), ws.numel(), nat.stream_handle()),
+              "forward_layer")
+    return out
+
+
+def forward_partial(hidden, model: MoEWeights, layer_index: int, assigned, weights):
+    """f32 sum of expert outputs without the residual; assigned < 0 skipped (EP helper)."""
+    torch = _torch()
+    s = model.spec
+    h = _hidden_bf16(hidden, s.d_model)
+    T = int(h.shape[0])
+    layer = model.native_layer(layer_index)
+    ws = _workspace(layer, T)
+    out = torch.empty((T, s.d_model), dtype=torch.float32, device="cuda")
+    nat.check(nat.lib().lynx_moe_forward_partial(ctypes_ref(layer), nat.ptr(h), T, nat.ptr(assigned),
+                                                 nat.ptr(weights), nat.ptr(out), nat.ptr(ws), ws.numel(),
+                                                 nat.stream_handle()), "forward_partial")
+    return out
+
+
+class LynxMoELayer:
+    """The whole decode MoE layer as one C call (lynx_moe_layer):
+
+        K0 router GEMV + RMSNorm -> K1 route + Lynx policy + remap ->
+        K2 histogram/scan permutation + gather -> K3 grouped expert GEMM
+        (tcgen05, used experts only) -> K4 weighted combine + residual.
+
+    Shapes are fixed at construction; buffers are preallocated, so calls
+    never synchronise the host and can be captured into a CUDA graph.
+    The selection/mask outputs stay on the device (``.expert_ids``,
+    ``.assigned``, ``.weights``, ``.retained_mask``, ``.flags`` ...).
+    """
+
+    def __init__(self, model: MoEWeights, layer_index: int, num_tokens: int,
+                 policy: PolicyConfig | None = None, phase: Phase = Phase.DECODE):
+        torch = _torch()
+        s = model.spec
+        self.model, self.layer_index, self.T = model, layer_index, int(num_tokens)
+        self.phase = phase
+        if policy is not None:
+            if phase is Phase.DECODE:
+                policy.resolved_min_experts(s.top_k)
+            self._pol = policy.to_native()
+        else:
+            self._pol = None
+        self._layer = model.native_layer(layer_index)
+        nbytes = int(nat.lib().lynx_moe_workspace_bytes(ctypes_ref(self._layer), self.T))
+        self.workspace = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+        T, N, k = self.T, s.num_experts, s.top_k
+        dev = "cuda"
+        self.expert_ids = torch.empty((T, k), dtype=torch.int32, device=dev)
+        self.probs = torch.empty((T, k), dtype=torch.float64, device=dev)
+        self.full_probs = torch.empty((T, N), dtype=torch.float64, device=dev)
+        self.conf = torch.empty((T,), dtype=torch.float64, device=dev)
+        self.counts = torch.empty((N,), dtype=torch.float64, device=dev)
+        self.retained_mask = torch.empty((N,), dtype=torch.uint8, device=dev)
+        self.assigned = torch.empty((T, k), dtype=torch.int32, device=dev)
+        self.weights = torch.empty((T, k), dtype=torch.float64, device=dev)
+        self.important = torch.empty((T,), dtype=torch.uint8, device=dev)
+        self.flags = torch.zeros((1,), dtype=torch.int32, device=dev)
+        self._sel = nat.LynxSelection(
+            expert_ids=nat.ptr(self.expert_ids), probs=nat.ptr(self.probs), full_probs=nat.ptr(self.full_probs),
+            conf=nat.ptr(self.conf), counts=nat.ptr(self.counts), retained=nat.ptr(self.retained_mask),
+            assigned=nat.ptr(self.assigned), weights=nat.ptr(self.weights), important=nat.ptr(self.important),
+            flags=nat.ptr(self.flags))
+        self._lib = nat.lib()
+        self._sel_ref = ctypes_ref(self._sel)
+        self._layer_ref = ctypes_ref(self._layer)
+        self._pol_ref = ctypes_ref(self._pol) if self._pol is not None else None
+
+    def __call__(self, hidden, out=None):
+        torch = _torch()
+        if hidden.dtype != torch.bfloat16 or not hidden.is_cuda or tuple(hidden.shape) != (
+                self.T, self.model.spec.d_model):
+            raise ValidationError(f"hidden must be a CUDA bf16 tensor of shape [{self.T}, "
+                                  f"{self.model.spec.d_model}]")
+        if out is None:
+            out = torch.empty_like(hidden)
+        st = self._lib.lynx_moe_layer(self._layer_ref, hidden.data_ptr(), self.T,
+                                      1 if self.phase is Phase.DECODE else 0, self._pol_ref, out.data_ptr(),
+                                      self._sel_ref, self.workspace.data_ptr(), self.workspace.numel(),
+                                      torch.cuda.current_stream().cuda_stream)
+        nat.check(st, "lynx_moe_layer")
+        return out
+
+    def used_experts(self) -> int:
+        """Experts with >= 1 assigned slot in the last call (host sync; reporting only)."""
+        torch = _torch()
+        N = self.model.spec.num_experts
+        return int((torch.bincount(self.assigned.flatten().long(), minlength=N) > 0).sum().item())
+
+    def mask(self) -> ExpertMask:
+        """The last call's ExpertMask (host sync)."""
+        torch = _torch()
+        flags = int(self.flags.item())
+        return ExpertMask(layer_index=self.layer_index, phase=self.phase,
+                          retained=torch.nonzero(self.retained_mask).flatten().long(),
+                          remap_original=self.expert_ids.clone(), remap_assigned=self.assigned.clone(),
+                          remap_weights=self.weights.clone(), clipped=bool(flags & nat.FLAG_CLIPPED),
+                          important_tokens=torch.nonzero(self.important).flatten().long())
