@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Lynx MoE decode layer benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lynx|reference] [--config c2]
+
+One step = one full MoE decode layer call on one batch: router GEMV+RMSNorm
+(K0) -> route + Lynx policy + remap (K1) -> permutation/gather (K2) ->
+grouped SwiGLU expert GEMM over the used experts on tcgen05 (K3) -> weighted
+combine + residual (K4).  Default workload (configs[1]): Mixtral-8x7B layer
+shape, d=4096, ff=14336, 8 experts, top-2, bf16, decode batch 32, Lynx
+latency policy dropping 4 experts.
+
+N > 1 (torchrun): expert parallel, rank g owns 8/N experts, 32 tokens per
+rank (weak scaling), NCCL all-gather of logits + all-to-all dispatch/combine.
+
+--impl reference: the reference's CPU algorithm (the oracle port of moetrim's
+route_batch + apply_policy + forward_layer with a SwiGLU expert, numpy/BLAS
+on all host cores) on the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE decode layer µs/step & tokens/s (Mixtral shape, bs32); % of HBM roofline"
+
+CONFIGS = {
+    # configs[1] of BASELINE.json -- the headline
+    "c2": dict(workload="mixtral-8x7b-moe-layer-decode-bs32-lynx-latency-drop4", d=4096, ff=14336, N=8, k=2,
+               T=32, mode="latency", drop=4, rotate=4),
+    "c2-nolynx": dict(workload="mixtral-8x7b-moe-layer-decode-bs32-no-lynx", d=4096, ff=14336, N=8, k=2, T=32,
+                      mode="latency", drop=0, rotate=4),
+    "c2-acc": dict(workload="mixtral-8x7b-moe-layer-decode-bs32-lynx-accuracy", d=4096, ff=14336, N=8, k=2,
+                   T=32, mode="accuracy", drop=0, rotate=4),
+    # configs[4]: Mixtral-8x22B expert-parallel shape (T is per rank)
+    "c5": dict(workload="mixtral-8x22b-moe-layer-decode-lynx-latency-drop4", d=6144, ff=16384, N=8, k=2, T=32,
+               mode="latency", drop=4, rotate=3),
+}
+
+SWIGLU_BYTES = lambda c: 3 * c["d"] * c["ff"] * 2  # noqa: E731
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - reporting only
+            log("clock sampler unavailable:", e)
+            self.nv = None
+
+    def _poll_once(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        for bit, name in self.REASONS.items():
+            if r & bit:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._poll_once()
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv is not None:
+            self._stop.set()
+            self._t.join()
+            if not self.samples:
+                self._poll_once()
+
+    def summary(self):
+        if self.nv is None:
+            return None
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ffn_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return None
+
+
+# ------------------------------------------------------------- CPU oracle
+def cpu_layer_setup(c, seed=0):
+    """Host-side C2 layer for the oracle port: fp32 weights of the experts the
+    sampled batches use (others are never read by the reference either)."""
+    import numpy as np
+
+    from oracle import lynx_oracle as O
+    rng = np.random.default_rng(seed)
+    T, d, ff, N, k = c["T"], c["d"], c["ff"], c["N"], c["k"]
+    router_w = (rng.standard_normal((d, N), dtype=np.float32) * (2.0 / np.sqrt(d))).astype(np.float32)
+    batches = [rng.standard_normal((T, d), dtype=np.float32) for _ in range(2)]
+    pol = O.Policy(mode=c["mode"], drop_count=c["drop"])
+    used = set()
+    for h in batches:
+        ids, probs, full = O.route(O.router_logits(h, router_w).astype(np.float64), k)
+        m = O.apply(ids, probs, full, pol)
+        used.update(int(e) for e in np.unique(m.assigned))
+    w1, w3, w2 = {}, {}, {}
+    for e in sorted(used):
+        w1[e] = rng.standard_normal((ff, d), dtype=np.float32) / np.float32(np.sqrt(d))
+        w3[e] = rng.standard_normal((ff, d), dtype=np.float32) / np.float32(np.sqrt(d))
+        w2[e] = rng.standard_normal((d, ff), dtype=np.float32) / np.float32(np.sqrt(ff))
+    return dict(router_w=router_w, batches=batches, pol=pol, w1=w1, w3=w3, w2=w2, k=k)
+
+
+def cpu_layer_step(st, i):
+    import numpy as np
+
+    from oracle import lynx_oracle as O
+    h = st["batches"][i % len(st["batches"])]
+    ids, probs, full = O.route(O.router_logits(h, st["router_w"]).astype(np.float64), st["k"])
+    m = O.apply(ids, probs, full, st["pol"])
+    return O.forward_swiglu(h, st["w1"], st["w3"], st["w2"], m.assigned, m.weights)
+
+
+def cpu_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def cpu_baseline(c, steps=3):
+    st = cpu_layer_setup(c)
+    cpu_layer_step(st, 0)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        cpu_layer_step(st, i)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": c["T"] / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+            "sample": f"{steps} full layer steps (T={c['T']}, router+route+{c['mode']} policy+SwiGLU fp32 over "
+                      f"the used experts) of the oracle port oracle/lynx_oracle.py, numpy/OpenBLAS",
+            "ms_per_step": dt * 1e3}
+
+
+# -------------------------------------------------------------- reference arm
+def run_reference(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    st = cpu_layer_setup(c)
+    for i in range(args.warmup):
+        cpu_layer_step(st, i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        cpu_layer_step(st, i)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = c["T"] / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": c["workload"], "d_model": c["d"], "d_ff": c["ff"], "experts": c["N"],
+                   "top_k": c["k"], "tokens": c["T"], "policy": f"{c['mode']} drop {c['drop']}",
+                   "parallelism": "host"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+                         "sample": "each step = one full layer step of the oracle port (moetrim's "
+                                   "route_batch/apply_policy/forward_layer restated, SwiGLU fp32)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- GPU arm
+def run_single(args, c):
+    import torch
+
+    import paper_2411_08982_b200 as L
+    T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
+    spec = L.MoEModelSpec(num_layers=n, num_experts=N, top_k=k, d_model=d, d_ff=ff)
+    model = L.build_swiglu_model(spec, seed=0)
+    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"])
+    layers = [L.LynxMoELayer(model, l, T, policy=pol) for l in range(n)]
+    g = torch.Generator(device="cuda").manual_seed(1)
+    hid = [torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
+    outs = [torch.empty_like(h) for h in hid]
+
+    for i in range(max(args.warmup, n)):
+        layers[i % n](hid[i % n], outs[i % n])
+    torch.cuda.synchronize()
+    used = [layers[l].used_experts() for l in range(n)]
+
+    # CUDA graphs: one per rotating layer copy
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for l in range(n):
+            layers[l](hid[l], outs[l])
+    torch.cuda.current_stream().wait_stream(side)
+    graphs = []
+    for l in range(n):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            layers[l](hid[l], outs[l])
+        graphs.append(gr)
+    for gr in graphs:
+        gr.replay()
+    torch.cuda.synchronize()
+
+    # (A) timed region: K graph replays, device-timed
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        torch.cuda.synchronize()
+        e0.record()
+        for i in range(args.steps):
+            graphs[i % n].replay()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+
+    # (B) per-kernel device time on the launching stream (events between K0..K4)
+    kp = min(args.steps, 100)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(kp)]
+    for i in range(kp):
+        layers[i % n].profiled(hid[i % n], evs[i], outs[i % n])
+    torch.cuda.synchronize()
+    names = ["router", "select", "permute", "ffn", "combine"]
+    kern = {nm: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(kp))
+            for j, nm in enumerate(names)}
+    step_b = statistics.mean(evs[i][0].elapsed_time(evs[i][5]) for i in range(kp))
+
+    # (C) end to end through the public API with pinned host buffers
+    h_host = [h.cpu().pin_memory() for h in hid]
+    o_host = [torch.empty_like(h_host[0]).pin_memory() for _ in range(n)]
+    for i in range(n):
+        hid[i].copy_(h_host[i], non_blocking=True)
+        layers[i](hid[i], outs[i])
+        o_host[i].copy_(outs[i], non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for i in range(args.steps):
+        l = i % n
+        hid[l].copy_(h_host[l], non_blocking=True)
+        layers[l](hid[l], outs[l])
+        o_host[l].copy_(outs[l], non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    ms_e2e = c0.elapsed_time(c1) / args.steps
+
+    # algorithmic bytes of one layer step (used experts only) and of one FFN launch
+    mean_used = statistics.mean(used[i % n] for i in range(kp))
+    ffn_bytes = mean_used * SWIGLU_BYTES(c)
+    step_bytes = ffn_bytes + N * d * 2 + 2 * T * d * 2
+    peak, peak_src = measured_peaks()
+    achieved = ffn_bytes / (kern["ffn"] * 1e-3) / 1e9
+    traffic = ncu_traffic()
+    result = {
+        "metric": METRIC, "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
+        "config": {"workload": c["workload"], "d_model": d, "d_ff": ff, "experts": N, "top_k": k,
+                   "global_batch": T, "tokens_per_gpu": T, "policy": f"{c['mode']} drop {c['drop']}",
+                   "parallelism": "single", "weight_copies": n,
+                   "l2": f"inputs > L2: {n} rotating layer copies "
+                         f"({n * N * SWIGLU_BYTES(c) / 1e9:.1f} GB) >> 126 MB L2",
+                   "used_experts_per_copy": used, "mean_used_experts": mean_used},
+        "roofline": {"bound": "hbm", "kernel": "ffn_kernel (K3, tcgen05 grouped SwiGLU)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_src,
+                     "frac_of_8TBs": achieved / 8000.0,
+                     "algorithmic_bytes_per_launch": ffn_bytes,
+                     "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
+                     "ffn_share_of_step": kern["ffn"] / step_b,
+                     "step_bytes": step_bytes, "step_achieved_gbs": step_bytes / (ms * 1e-3) / 1e9},
+        "kernel_ms": kern, "profiled_step_ms": step_b,
+        "e2e": {"value": T / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
+                "api": "paper_2411_08982_b200.LynxMoELayer.__call__ (lynx_moe_layer C ABI), eager"},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clocks.summary(),
+    }
+    return result
+
+
+def run_ep(args, c, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_08982_b200 as L
+    from paper_2411_08982_b200 import ep as EP
+    T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
+    if N % world:
+        raise SystemExit(f"{N} experts do not shard over {world} GPUs")
+    shape = EP.EPShape(num_experts=N, top_k=k, d_model=d, d_ff=ff, tokens_per_rank=T, world_size=world, rank=rank)
+    spec = L.MoEModelSpec(num_layers=1, num_experts=N, top_k=k, d_model=d, d_ff=ff)
+    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"])
+    ops = []
+    for l in range(n):
+        full = L.build_swiglu_model(spec, seed=100 + l)  # same seed on every rank -> identical model
+        w13 = EP.shard_experts(full.w13[0], rank, world)
+        w2 = EP.shard_experts(full.w2[0], rank, world)
+        ops.append(EP.NativeEPOps(shape, full.router_wt[0].contiguous(), w13, w2, pol))
+        del full
+        torch.cuda.empty_cache()
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    hid = [torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
+    for i in range(max(args.warmup, n)):
+        EP.ep_layer(shape, ops[i % n], hid[i % n])
+    torch.cuda.synchronize()
+    used_local = []
+    for l in range(n):
+        EP.ep_layer(shape, ops[l], hid[l])
+        a = ops[l].assigned_local
+        used_local.append(int((torch.bincount(a[a >= 0].long(), minlength=shape.experts_per_rank) > 0).sum()))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for i in range(args.steps):
+            EP.ep_layer(shape, ops[i % n], hid[i % n])
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    crit = torch.tensor([statistics.mean(used_local)], device="cuda")
+    tot = crit.clone()
+    dist.all_reduce(crit, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+
+    # e2e: host-resident inputs/outputs per step
+    h_host = [h.cpu().pin_memory() for h in hid]
+    o_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for i in range(args.steps):
+        l = i % n
+        hid[l].copy_(h_host[l], non_blocking=True)
+        out = EP.ep_layer(shape, ops[l], hid[l])
+        o_host.copy_(out, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    me = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+    dist.all_reduce(me, op=dist.ReduceOp.MAX)
+    ms_e2e = float(me.item())
+    Tg = T * world
+    peak, peak_src = measured_peaks()
+    crit_bytes = float(crit.item()) * SWIGLU_BYTES(c)
+    return {
+        "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
+        "config": {"workload": c["workload"] + f"-ep{world}", "d_model": d, "d_ff": ff, "experts": N,
+                   "top_k": k, "global_batch": Tg, "tokens_per_gpu": T, "policy": f"{c['mode']} drop {c['drop']}",
+                   "parallelism": f"ep{world}", "weight_copies": n,
+                   "mean_used_experts_total": float(tot.item()), "critical_path_used_experts": float(crit.item())},
+        "roofline": {"bound": "hbm", "kernel": "ffn_kernel per rank (critical path)",
+                     "achieved": crit_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": crit_bytes / (ms * 1e-3) / 1e9 / peak, "peak_source": peak_src,
+                     "note": "critical-path bytes / whole step time (includes NCCL)", "traffic": None},
+        "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
+        "gpu_launches": 7 * args.steps,
+        "clocks": clocks.summary(),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["lynx", "reference"], default="lynx")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, c)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        result = run_ep(args, c, rank, world, local_rank)
+    else:
+        result = run_single(args, c)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(c)
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

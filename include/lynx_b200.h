@@ -192,6 +192,17 @@ int lynx_moe_layer(const lynx_layer_t *layer, const uint16_t *hidden, int T, int
                    const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,
                    void *workspace, size_t workspace_bytes, lynx_stream_t stream);
 
+/* lynx_moe_layer that also records caller-created CUDA events (cudaEvent_t)
+ * on `stream` around each kernel: events[0] before K0 (router), [1] before
+ * K1 (select), [2] before K2 (permute), [3] before K3 (expert FFN), [4]
+ * before K4 (combine), [5] after K4.  n_events must be LYNX_PROFILE_EVENTS.
+ * Used by bench.py to time the FFN kernel on the launching stream. */
+#define LYNX_PROFILE_EVENTS 6
+int lynx_moe_layer_profiled(const lynx_layer_t *layer, const uint16_t *hidden, int T, int decode,
+                            const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,
+                            void *workspace, size_t workspace_bytes, lynx_stream_t stream,
+                            void *const *events, int n_events);
+
 /* Pack HF-layout gate/up projections w1, w3 [N, ff, d] into the
  * interleaved w13 layout the SwiGLU kernel streams. */
 int lynx_pack_w13(const uint16_t *w1, const uint16_t *w3, int N, int ff, int d, uint16_t *w13,

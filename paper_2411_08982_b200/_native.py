@@ -75,6 +75,7 @@ _SIGS = {
     "lynx_moe_forward": (_i, [_p, _p, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_forward_partial": (_i, [_p, _p, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_layer": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "lynx_moe_layer_profiled": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p, _p, _i]),
     "lynx_pack_w13": (_i, [_p, _p, _i, _i, _i, _p, _p]),
     "lynx_ep_pack": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "lynx_ep_local_mask": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p]),

@@ -158,10 +158,12 @@ T* at(void* base, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(base) + off);
 }
 
-int check_layer(const lynx_layer_t* L, int T) {
+// slots_exceed_ok: an expert-parallel shard holds fewer experts than the
+// routing width; its mask has top_k slots per token, most of them -1.
+int check_layer(const lynx_layer_t* L, int T, bool slots_exceed_ok = false) {
   if (!L) return LYNX_ERR_SHAPE;
   if (T < 1 || L->num_experts < 1 || L->d_model < 8 || L->d_ff < 8) return LYNX_ERR_SHAPE;
-  if (L->top_k < 1 || L->top_k > L->num_experts) return LYNX_ERR_TOPK;
+  if (L->top_k < 1 || (!slots_exceed_ok && L->top_k > L->num_experts)) return LYNX_ERR_TOPK;
   if (L->num_experts > LYNX_MAX_EXPERTS || L->top_k > LYNX_MAX_TOPK || T > LYNX_MAX_TOKENS)
     return LYNX_ERR_UNSUPPORTED;
   if (L->d_model % 8 || L->d_ff % 8) return LYNX_ERR_UNSUPPORTED;  // TMA 16-byte strides
@@ -194,9 +196,10 @@ int check_policy(const lynx_policy_t* pol, int N, int k, int decode, int* floor_
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? LYNX_OK : LYNX_ERR_CUDA; }
 
 // K2 -> K3 -> K4 for a given mask (assigned/weights in device memory).
+// ev (optional): events recorded before K2, K3, K4 and after K4.
 int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int32_t* assigned,
                  const double* weights, uint16_t* out_bf16, float* out_f32, void* ws, const Plan& P,
-                 cudaStream_t s) {
+                 cudaStream_t s, cudaEvent_t const* ev = nullptr) {
   const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
@@ -229,6 +232,7 @@ int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int
   pa.out = dv;
   pa.counters = counters;
   pa.n_counters = P.n_counters;
+  if (ev) cudaEventRecord(ev[0], s);
   int st = cuda_status(launch_permute(pa, sms, s));
   if (st) return st;
 
@@ -261,8 +265,10 @@ int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int
   fp.kb2_per = g.kb2_per;
   fp.kb2_total = g.kb2_total;
   fp.rows_cap = c.rows_cap;
+  if (ev) cudaEventRecord(ev[1], s);
   st = cuda_status(launch_ffn(fp, g.bn, sms, s));
   if (st) return st;
+  if (ev) cudaEventRecord(ev[2], s);
 
   CombineArgs ca;
   ca.hidden = out_f32 ? nullptr : hidden;
@@ -276,7 +282,9 @@ int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int
   ca.tok_weight = dv.tok_weight;
   ca.out_bf16 = out_bf16;
   ca.out_f32 = out_f32;
-  return cuda_status(launch_combine(ca, s));
+  st = cuda_status(launch_combine(ca, s));
+  if (!st && ev) cudaEventRecord(ev[3], s);
+  return st;
 }
 
 void* aligned_ws(void* ws) {
@@ -474,7 +482,7 @@ int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t*
 static int moe_forward_common(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
                               const double* weights, uint16_t* out_bf16, float* out_f32, void* workspace,
                               size_t workspace_bytes, lynx_stream_t stream) {
-  int st = check_layer(layer, T);
+  int st = check_layer(layer, T, out_f32 != nullptr);
   if (st) return st;
   const Plan P = plan_for(layer, T, false);
   if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
@@ -496,9 +504,9 @@ int lynx_moe_forward_partial(const lynx_layer_t* layer, const uint16_t* hidden, 
                             stream);
 }
 
-int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
-                   uint16_t* out, const lynx_selection_t* sel, void* workspace, size_t workspace_bytes,
-                   lynx_stream_t stream) {
+static int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode,
+                          const lynx_policy_t* policy, uint16_t* out, const lynx_selection_t* sel, void* workspace,
+                          size_t workspace_bytes, lynx_stream_t stream, cudaEvent_t const* ev) {
   int st = check_layer(layer, T);
   if (st) return st;
   if (!layer->router_wt) return LYNX_ERR_SHAPE;
@@ -511,6 +519,7 @@ int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   void* ws = aligned_ws(workspace);
 
   double* logits = at<double>(ws, P.logits);
+  if (ev) cudaEventRecord(ev[0], stream);
   st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, logits, stream));
   if (st) return st;
 
@@ -539,9 +548,24 @@ int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   a.important = LYNX_PICK(important, important, uint8_t);
   a.flags = LYNX_PICK(flags, flags, int32_t);
 #undef LYNX_PICK
+  if (ev) cudaEventRecord(ev[1], stream);
   st = cuda_status(launch_route_select(a, stream));
   if (st) return st;
-  return forward_impl(layer, hidden, T, a.assigned, a.weights, out, nullptr, ws, P, stream);
+  return forward_impl(layer, hidden, T, a.assigned, a.weights, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr);
+}
+
+int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
+                   uint16_t* out, const lynx_selection_t* sel, void* workspace, size_t workspace_bytes,
+                   lynx_stream_t stream) {
+  return moe_layer_impl(layer, hidden, T, decode, policy, out, sel, workspace, workspace_bytes, stream, nullptr);
+}
+
+int lynx_moe_layer_profiled(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode,
+                            const lynx_policy_t* policy, uint16_t* out, const lynx_selection_t* sel, void* workspace,
+                            size_t workspace_bytes, lynx_stream_t stream, void* const* events, int n_events) {
+  if (!events || n_events != LYNX_PROFILE_EVENTS) return LYNX_ERR_SHAPE;
+  return moe_layer_impl(layer, hidden, T, decode, policy, out, sel, workspace, workspace_bytes, stream,
+                        reinterpret_cast<cudaEvent_t const*>(events));
 }
 
 int lynx_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,

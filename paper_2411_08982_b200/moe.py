@@ -291,6 +291,25 @@ class LynxMoELayer:
         nat.check(st, "lynx_moe_layer")
         return out
 
+    def profiled(self, hidden, events, out=None):
+        """__call__ that records 6 torch.cuda.Events around K0..K4 (lynx_moe_layer_profiled)."""
+        torch = _torch()
+        if out is None:
+            out = torch.empty_like(hidden)
+        stream = torch.cuda.current_stream()
+        handles = (ctypes.c_void_p * 6)()
+        for i, ev in enumerate(events):
+            if not ev.cuda_event:
+                ev.record(stream)  # torch creates CUDA events lazily
+            handles[i] = ev.cuda_event
+        st = self._lib.lynx_moe_layer_profiled(self._layer_ref, hidden.data_ptr(), self.T,
+                                               1 if self.phase is Phase.DECODE else 0, self._pol_ref,
+                                               out.data_ptr(), self._sel_ref, self.workspace.data_ptr(),
+                                               self.workspace.numel(), stream.cuda_stream,
+                                               ctypes.cast(handles, ctypes.c_void_p), 6)
+        nat.check(st, "lynx_moe_layer_profiled")
+        return out
+
     def used_experts(self) -> int:
         """Experts with >= 1 assigned slot in the last call (host sync; reporting only)."""
         torch = _torch()
