@@ -121,6 +121,7 @@ typedef struct lynx_layer {
 typedef struct lynx_dispatch {
   int32_t *n_seg;       /* [1]  number of segments (used experts split at LYNX_SEG_ROWS) */
   int32_t *n_used;      /* [1]  number of used experts */
+  int32_t *n_rows;      /* [1]  permuted rows in use (each expert padded to 16) */
   int32_t *seg_expert;  /* [max_seg] expert id of each segment */
   int32_t *seg_row;     /* [max_seg] first permuted row (16-aligned) */
   int32_t *seg_count;   /* [max_seg] token rows in the segment */
@@ -169,11 +170,12 @@ int lynx_remap(const int32_t *expert_ids, const double *full_probs, int T, int N
                const uint8_t *retained, int32_t *assigned, double *weights, int32_t *flags,
                lynx_stream_t stream);
 
-/* ---- K2: histogram + scan permutation and gather (simulator.py:104-112) */
+/* ---- K2: dispatch plan (bitmap histogram + scan, simulator.py:104-112)
+ * and gather of the token rows into expert segments */
 int lynx_permute(const int32_t *assigned, const double *weights, const uint16_t *hidden,
                  int T, int N, int k, int d, const lynx_dispatch_t *out, lynx_stream_t stream);
 
-/* ---- K3+K4: grouped expert FFN over used experts + weighted combine ---
+/* ---- K3: grouped expert FFN over used experts + fused weighted combine --
  * forward_layer(hidden, model, layer, mask) for a given mask. */
 int lynx_moe_forward(const lynx_layer_t *layer, const uint16_t *hidden, int T,
                      const int32_t *assigned, const double *weights, uint16_t *out,
@@ -185,7 +187,7 @@ int lynx_moe_forward_partial(const lynx_layer_t *layer, const uint16_t *hidden, 
                              const int32_t *assigned, const double *weights, float *partial_out,
                              void *workspace, size_t workspace_bytes, lynx_stream_t stream);
 
-/* ---- whole decode layer: K0 -> K1 -> K2 -> K3 -> K4 ------------------
+/* ---- whole decode layer: K0 -> K1 -> K2 -> K3 -------------------------
  * _apply_routing + forward_layer (simulator.py:245-266, 86-113).
  * `sel` may be NULL; when given, the selection/mask outputs are copied out. */
 int lynx_moe_layer(const lynx_layer_t *layer, const uint16_t *hidden, int T, int decode,
@@ -194,9 +196,10 @@ int lynx_moe_layer(const lynx_layer_t *layer, const uint16_t *hidden, int T, int
 
 /* lynx_moe_layer that also records caller-created CUDA events (cudaEvent_t)
  * on `stream` around each kernel: events[0] before K0 (router), [1] before
- * K1 (select), [2] before K2 (permute), [3] before K3 (expert FFN), [4]
- * before K4 (combine), [5] after K4.  n_events must be LYNX_PROFILE_EVENTS.
- * Used by bench.py to time the FFN kernel on the launching stream. */
+ * K1 (select + plan), [2] before K2 (gather), [3] before K3 (expert FFN with
+ * the fused combine), [4] after K3, [5] at the end.  n_events must be
+ * LYNX_PROFILE_EVENTS.  Event records serialise the programmatic launches,
+ * so bench.py uses this only to attribute time to kernels. */
 #define LYNX_PROFILE_EVENTS 6
 int lynx_moe_layer_profiled(const lynx_layer_t *layer, const uint16_t *hidden, int T, int decode,
                             const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 
 # include/lynx_b200.h constants
 LYNX_OK = 0
+ABI_VERSION = 2
 STATUS = {
     -1: "invalid shape", -2: "k out of range", -3: "min_experts must be >= top_k",
     -4: "retained set empty or out of range", -5: "token count mismatch", -6: "CUDA error",
@@ -56,7 +57,7 @@ class LynxLayer(ctypes.Structure):
 
 class LynxDispatch(ctypes.Structure):
     _fields_ = [(name, _p) for name in (
-        "n_seg", "n_used", "seg_expert", "seg_row", "seg_count", "perm_token", "perm_weight",
+        "n_seg", "n_used", "n_rows", "seg_expert", "seg_row", "seg_count", "perm_token", "perm_weight",
         "tok_rows", "tok_weight", "x_perm")]
 
 
@@ -102,7 +103,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.lynx_abi_version() != 1:
+        if lib.lynx_abi_version() != ABI_VERSION:
             raise NativeLibraryError("liblynx_b200.so ABI version mismatch")
         _lib = lib
         return lib

@@ -1,6 +1,11 @@
 // capi.cu -- extern "C" entry points of include/lynx_b200.h: argument
 // validation mirroring the reference's ValidationError sites, workspace
-// planning, TMA descriptor encoding and the K0..K4 launch sequence.
+// planning, TMA descriptor encoding and the kernel chain
+//
+//   K0 router GEMV -> K1 route + policy + remap + dispatch plan ->
+//   K2 gather -> K3 grouped expert GEMM (tcgen05) + fused combine
+//
+// launched back to back with programmatic dependent launch (no host sync).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -15,7 +20,7 @@ using namespace lynx;
 
 namespace {
 
-constexpr int kAbiVersion = 1;
+constexpr int kAbiVersion = 2;
 
 int sm_count_cached() {
   static int cached_dev = -1, cached = 0;
@@ -60,6 +65,7 @@ bool encode_bf16(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// k blocks (64 wide) per phase-1 unit: 32 -> 512 KB of W2 per unit.
 int kb2_per_unit() {
   static int v = 0;
   if (!v) {
@@ -105,8 +111,8 @@ Geometry geometry(const lynx_layer_t* L, int T) {
 // Workspace carve-up.  Selection region only for the whole-layer call.
 struct Plan {
   size_t logits, ids, probs, full, conf, counts, retained, assigned, weights, important, flags;
-  size_t n_seg, n_used, seg_expert, seg_row, seg_count, perm_token, perm_weight, tok_rows, tok_weight;
-  size_t counters, x_perm, h, partial;
+  size_t n_seg, n_used, n_rows, seg_expert, seg_row, seg_count, perm_token, perm_weight, tok_rows, tok_weight;
+  size_t counters, x_perm, h, y;
   size_t total;
   int n_counters;
 };
@@ -137,6 +143,7 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   }
   p.n_seg = take(sizeof(int32_t));
   p.n_used = take(sizeof(int32_t));
+  p.n_rows = take(sizeof(int32_t));
   p.seg_expert = take(sizeof(int32_t) * c.max_seg);
   p.seg_row = take(sizeof(int32_t) * c.max_seg);
   p.seg_count = take(sizeof(int32_t) * c.max_seg);
@@ -144,11 +151,13 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.perm_weight = take(sizeof(float) * c.rows_cap);
   p.tok_rows = take(sizeof(int32_t) * T * k);
   p.tok_weight = take(sizeof(float) * T * k);
-  p.n_counters = 1 + c.max_seg;
+  // ticket + phase-0 done per segment + split chain per (segment, m-tile) +
+  // segments done per (m-tile, warp quarter)
+  p.n_counters = 1 + c.max_seg + c.max_seg * g.tiles2 + g.tiles2 * 4;
   p.counters = take(sizeof(int32_t) * p.n_counters);
   p.x_perm = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * d);
   p.h = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * ff);
-  p.partial = take(sizeof(float) * static_cast<size_t>(g.split2) * c.rows_cap * d);
+  p.y = take(sizeof(float) * static_cast<size_t>(c.rows_cap) * d);
   p.total = off + 256;  // slack for base alignment
   return p;
 }
@@ -174,7 +183,7 @@ int check_layer(const lynx_layer_t* L, int T, bool slots_exceed_ok = false) {
 
 // PolicyConfig.__post_init__ (policy.py:40-55) + the checks the reference
 // performs lazily on the decode path (policy.py:61-64, 130-133).
-int check_policy(const lynx_policy_t* pol, int N, int k, int decode, int* floor_keep) {
+int check_policy(const lynx_policy_t* pol, int k, int decode, int* floor_keep) {
   *floor_keep = k;
   if (!pol || pol->mode == LYNX_POLICY_NONE) return LYNX_OK;
   if (pol->mode != LYNX_POLICY_LATENCY && pol->mode != LYNX_POLICY_ACCURACY) return LYNX_ERR_CONFIG;
@@ -189,51 +198,53 @@ int check_policy(const lynx_policy_t* pol, int N, int k, int decode, int* floor_
   if (pol->min_experts > 0 && pol->min_experts < k) return LYNX_ERR_MIN_EXPERTS;
   if (pol->n_rank_weights != 0 && pol->n_rank_weights != k) return LYNX_ERR_CONFIG;
   if (pol->min_experts > 0) *floor_keep = pol->min_experts;
-  (void)N;
   return LYNX_OK;
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? LYNX_OK : LYNX_ERR_CUDA; }
 
-// K2 -> K3 -> K4 for a given mask (assigned/weights in device memory).
-// ev (optional): events recorded before K2, K3, K4 and after K4.
-int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int32_t* assigned,
-                 const double* weights, uint16_t* out_bf16, float* out_f32, void* ws, const Plan& P,
-                 cudaStream_t s, cudaEvent_t const* ev = nullptr) {
+PlanOut plan_out(void* ws, const Plan& P) {
+  PlanOut o;
+  o.enabled = 1;
+  o.n_seg = at<int32_t>(ws, P.n_seg);
+  o.n_used = at<int32_t>(ws, P.n_used);
+  o.n_rows = at<int32_t>(ws, P.n_rows);
+  o.seg_expert = at<int32_t>(ws, P.seg_expert);
+  o.seg_row = at<int32_t>(ws, P.seg_row);
+  o.seg_count = at<int32_t>(ws, P.seg_count);
+  o.perm_token = at<int32_t>(ws, P.perm_token);
+  o.perm_weight = at<float>(ws, P.perm_weight);
+  o.tok_rows = at<int32_t>(ws, P.tok_rows);
+  o.tok_weight = at<float>(ws, P.tok_weight);
+  o.counters = at<int>(ws, P.counters);
+  o.n_counters = P.n_counters;
+  return o;
+}
+
+inline void record(cudaEvent_t const* ev, int i, cudaStream_t s) {
+  if (ev) cudaEventRecord(ev[i], s);
+}
+
+// K2 gather -> K3 expert GEMM + combine, on a plan already in the workspace.
+// ev (optional): [0] before K2, [1] before K3, [2] after K3.
+int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_t* out_bf16, float* out_f32,
+                   void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev) {
   const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
   const Caps c = caps_for(T, N, k);
   const Geometry g = geometry(L, T);
+  const PlanOut o = plan_out(ws, P);
 
-  DispatchView dv;
-  dv.n_seg = at<int32_t>(ws, P.n_seg);
-  dv.n_used = at<int32_t>(ws, P.n_used);
-  dv.seg_expert = at<int32_t>(ws, P.seg_expert);
-  dv.seg_row = at<int32_t>(ws, P.seg_row);
-  dv.seg_count = at<int32_t>(ws, P.seg_count);
-  dv.perm_token = at<int32_t>(ws, P.perm_token);
-  dv.perm_weight = at<float>(ws, P.perm_weight);
-  dv.tok_rows = at<int32_t>(ws, P.tok_rows);
-  dv.tok_weight = at<float>(ws, P.tok_weight);
-  dv.x_perm = at<uint16_t>(ws, P.x_perm);
-  int* counters = at<int>(ws, P.counters);
-
-  PermuteArgs pa;
-  pa.assigned = assigned;
-  pa.weights = weights;
-  pa.hidden = hidden;
-  pa.T = T;
-  pa.N = N;
-  pa.k = k;
-  pa.d = d;
-  pa.max_seg = c.max_seg;
-  pa.rows_cap = c.rows_cap;
-  pa.out = dv;
-  pa.counters = counters;
-  pa.n_counters = P.n_counters;
-  if (ev) cudaEventRecord(ev[0], s);
-  int st = cuda_status(launch_permute(pa, sms, s));
+  GatherArgs ga;
+  ga.hidden = hidden;
+  ga.perm_token = o.perm_token;
+  ga.n_rows = o.n_rows;
+  ga.rows_cap = c.rows_cap;
+  ga.d = d;
+  ga.x_perm = at<uint16_t>(ws, P.x_perm);
+  record(ev, 0, s);
+  int st = cuda_status(launch_gather(ga, sms, s));
   if (st) return st;
 
   FfnParams fp;
@@ -245,16 +256,17 @@ int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int
     const uint32_t bw[3] = {64, 128, 1};
     const uint32_t ba[2] = {64, 16};
     if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw) ||
-        !encode_bf16(&fp.map_x, dv.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
+        !encode_bf16(&fp.map_x, ga.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
       return LYNX_ERR_CUDA;
   }
-  fp.n_seg = dv.n_seg;
-  fp.seg_expert = dv.seg_expert;
-  fp.seg_row = dv.seg_row;
-  fp.seg_count = dv.seg_count;
+  fp.n_seg = o.n_seg;
+  fp.seg_expert = o.seg_expert;
+  fp.seg_row = o.seg_row;
+  fp.seg_count = o.seg_count;
   fp.h = at<uint16_t>(ws, P.h);
-  fp.partial = at<float>(ws, P.partial);
-  fp.counters = counters;
+  fp.partial = at<float>(ws, P.y);
+  fp.counters = o.counters;
+  fp.max_seg = c.max_seg;
   fp.d = d;
   fp.ff = ff;
   fp.act = L->activation;
@@ -265,30 +277,107 @@ int forward_impl(const lynx_layer_t* L, const uint16_t* hidden, int T, const int
   fp.kb2_per = g.kb2_per;
   fp.kb2_total = g.kb2_total;
   fp.rows_cap = c.rows_cap;
-  if (ev) cudaEventRecord(ev[1], s);
+  fp.T = T;
+  fp.k = k;
+  fp.hidden = out_f32 ? nullptr : hidden;
+  fp.tok_rows = o.tok_rows;
+  fp.tok_weight = o.tok_weight;
+  fp.out_bf16 = out_bf16;
+  fp.out_f32 = out_f32;
+  record(ev, 1, s);
   st = cuda_status(launch_ffn(fp, g.bn, sms, s));
-  if (st) return st;
-  if (ev) cudaEventRecord(ev[2], s);
-
-  CombineArgs ca;
-  ca.hidden = out_f32 ? nullptr : hidden;
-  ca.partial = fp.partial;
-  ca.split2 = g.split2;
-  ca.rows_cap = c.rows_cap;
-  ca.T = T;
-  ca.k = k;
-  ca.d = d;
-  ca.tok_rows = dv.tok_rows;
-  ca.tok_weight = dv.tok_weight;
-  ca.out_bf16 = out_bf16;
-  ca.out_f32 = out_f32;
-  st = cuda_status(launch_combine(ca, s));
-  if (!st && ev) cudaEventRecord(ev[3], s);
+  record(ev, 2, s);
   return st;
 }
 
 void* aligned_ws(void* ws) {
   return reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+}
+
+SelectArgs select_args(const double* logits, int T, int N, int k, int decode, const lynx_policy_t* policy,
+                       int floor_keep) {
+  SelectArgs a{};
+  a.logits = logits;
+  a.T = T;
+  a.N = N;
+  a.k = k;
+  a.decode = decode;
+  if (policy) {
+    a.pol = *policy;
+  } else {
+    a.pol = lynx_policy_t{};
+    a.pol.mode = LYNX_POLICY_NONE;
+  }
+  a.floor_keep = floor_keep;
+  a.plan.enabled = 0;
+  return a;
+}
+
+int moe_forward_common(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
+                       const double* weights, uint16_t* out_bf16, float* out_f32, void* workspace,
+                       size_t workspace_bytes, cudaStream_t stream) {
+  int st = check_layer(layer, T, out_f32 != nullptr);
+  if (st) return st;
+  const Plan P = plan_for(layer, T, false);
+  if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
+  void* ws = aligned_ws(workspace);
+  st = cuda_status(launch_plan(assigned, weights, T, layer->num_experts, layer->top_k, plan_out(ws, P), stream));
+  if (st) return st;
+  return gather_and_ffn(layer, hidden, T, out_bf16, out_f32, ws, P, stream, nullptr);
+}
+
+int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
+                   uint16_t* out, const lynx_selection_t* sel, void* workspace, size_t workspace_bytes,
+                   cudaStream_t stream, cudaEvent_t const* ev) {
+  int st = check_layer(layer, T);
+  if (st) return st;
+  if (!layer->router_wt) return LYNX_ERR_SHAPE;
+  const int N = layer->num_experts, k = layer->top_k;
+  int floor_keep = k;
+  st = check_policy(policy, k, decode, &floor_keep);
+  if (st) return st;
+  const Plan P = plan_for(layer, T, true);
+  if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
+  void* ws = aligned_ws(workspace);
+
+  double* logits = at<double>(ws, P.logits);
+  record(ev, 0, stream);
+  st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, logits, stream));
+  if (st) return st;
+
+  SelectArgs a = select_args(logits, T, N, k, decode, policy, floor_keep);
+  a.stage = select_can_stage(T, N, k, true) ? 1 : 0;
+#define LYNX_PICK(field, off, type) ((sel && sel->field) ? sel->field : at<type>(ws, P.off))
+  a.ids = LYNX_PICK(expert_ids, ids, int32_t);
+  a.probs = LYNX_PICK(probs, probs, double);
+  a.full = LYNX_PICK(full_probs, full, double);
+  a.conf = LYNX_PICK(conf, conf, double);
+  a.counts = LYNX_PICK(counts, counts, double);
+  a.retained = LYNX_PICK(retained, retained, uint8_t);
+  a.assigned = LYNX_PICK(assigned, assigned, int32_t);
+  a.weights = LYNX_PICK(weights, weights, double);
+  a.important = LYNX_PICK(important, important, uint8_t);
+  a.flags = LYNX_PICK(flags, flags, int32_t);
+#undef LYNX_PICK
+  a.plan = plan_out(ws, P);
+  record(ev, 1, stream);
+  st = cuda_status(launch_route_select(a, stream));
+  if (st) return st;
+  st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr);
+  record(ev, 5, stream);
+  return st;
+}
+
+int route_select_common(SelectArgs a, const lynx_selection_t* out, cudaStream_t stream) {
+  a.conf = out->conf;
+  a.counts = out->counts;
+  a.retained = out->retained;
+  a.assigned = out->assigned;
+  a.weights = out->weights;
+  a.important = out->important;
+  a.flags = out->flags;
+  a.stage = select_can_stage(a.T, a.N, a.k, false) ? 1 : 0;
+  return cuda_status(launch_route_select(a, stream));
 }
 
 }  // namespace
@@ -353,32 +442,13 @@ int lynx_route_select(const double* logits, int T, int N, int k, int decode, con
       !out->weights || !out->flags)
     return LYNX_ERR_SHAPE;
   int floor_keep = k;
-  const int st = check_policy(policy, N, k, decode, &floor_keep);
+  const int st = check_policy(policy, k, decode, &floor_keep);
   if (st) return st;
-  SelectArgs a;
-  a.logits = logits;
-  a.T = T;
-  a.N = N;
-  a.k = k;
-  a.decode = decode;
-  if (policy) {
-    a.pol = *policy;
-  } else {
-    a.pol = lynx_policy_t{};
-    a.pol.mode = LYNX_POLICY_NONE;
-  }
-  a.floor_keep = floor_keep;
+  SelectArgs a = select_args(logits, T, N, k, decode, policy, floor_keep);
   a.ids = out->expert_ids;
   a.probs = out->probs;
   a.full = out->full_probs;
-  a.conf = out->conf;
-  a.counts = out->counts;
-  a.retained = out->retained;
-  a.assigned = out->assigned;
-  a.weights = out->weights;
-  a.important = out->important;
-  a.flags = out->flags;
-  return cuda_status(launch_route_select(a, stream));
+  return route_select_common(a, out, stream);
 }
 
 int lynx_apply_policy(const int32_t* expert_ids, const double* probs, const double* full_probs, int T, int N, int k,
@@ -389,32 +459,13 @@ int lynx_apply_policy(const int32_t* expert_ids, const double* probs, const doub
   if (!out || !expert_ids || !probs || !full_probs || !out->conf || !out->assigned || !out->weights || !out->flags)
     return LYNX_ERR_SHAPE;
   int floor_keep = k;
-  const int st = check_policy(policy, N, k, decode, &floor_keep);
+  const int st = check_policy(policy, k, decode, &floor_keep);
   if (st) return st;
-  SelectArgs a;
-  a.logits = nullptr;
-  a.T = T;
-  a.N = N;
-  a.k = k;
-  a.decode = decode;
-  if (policy) {
-    a.pol = *policy;
-  } else {
-    a.pol = lynx_policy_t{};
-    a.pol.mode = LYNX_POLICY_NONE;
-  }
-  a.floor_keep = floor_keep;
+  SelectArgs a = select_args(nullptr, T, N, k, decode, policy, floor_keep);
   a.ids = const_cast<int32_t*>(expert_ids);
   a.probs = const_cast<double*>(probs);
   a.full = const_cast<double*>(full_probs);
-  a.conf = out->conf;
-  a.counts = out->counts;
-  a.retained = out->retained;
-  a.assigned = out->assigned;
-  a.weights = out->weights;
-  a.important = out->important;
-  a.flags = out->flags;
-  return cuda_status(launch_route_select(a, stream));
+  return route_select_common(a, out, stream);
 }
 
 int lynx_topk(const double* values, int T, int N, int k, int32_t* ids, double* out, lynx_stream_t stream) {
@@ -454,39 +505,30 @@ int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t*
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
   const Caps c = caps_for(T, N, k);
-  PermuteArgs pa;
-  pa.assigned = assigned;
-  pa.weights = weights;
-  pa.hidden = hidden;
-  pa.T = T;
-  pa.N = N;
-  pa.k = k;
-  pa.d = d;
-  pa.max_seg = c.max_seg;
-  pa.rows_cap = c.rows_cap;
-  pa.out.n_seg = out->n_seg;
-  pa.out.n_used = out->n_used;
-  pa.out.seg_expert = out->seg_expert;
-  pa.out.seg_row = out->seg_row;
-  pa.out.seg_count = out->seg_count;
-  pa.out.perm_token = out->perm_token;
-  pa.out.perm_weight = out->perm_weight;
-  pa.out.tok_rows = out->tok_rows;
-  pa.out.tok_weight = out->tok_weight;
-  pa.out.x_perm = out->x_perm;
-  pa.counters = nullptr;
-  pa.n_counters = 0;
-  return cuda_status(launch_permute(pa, sms, stream));
-}
-
-static int moe_forward_common(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
-                              const double* weights, uint16_t* out_bf16, float* out_f32, void* workspace,
-                              size_t workspace_bytes, lynx_stream_t stream) {
-  int st = check_layer(layer, T, out_f32 != nullptr);
+  PlanOut o;
+  o.enabled = 1;
+  o.n_seg = out->n_seg;
+  o.n_used = out->n_used;
+  o.n_rows = out->n_rows;
+  o.seg_expert = out->seg_expert;
+  o.seg_row = out->seg_row;
+  o.seg_count = out->seg_count;
+  o.perm_token = out->perm_token;
+  o.perm_weight = out->perm_weight;
+  o.tok_rows = out->tok_rows;
+  o.tok_weight = out->tok_weight;
+  o.counters = nullptr;
+  o.n_counters = 0;
+  int st = cuda_status(launch_plan(assigned, weights, T, N, k, o, stream));
   if (st) return st;
-  const Plan P = plan_for(layer, T, false);
-  if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
-  return forward_impl(layer, hidden, T, assigned, weights, out_bf16, out_f32, aligned_ws(workspace), P, stream);
+  GatherArgs ga;
+  ga.hidden = hidden;
+  ga.perm_token = out->perm_token;
+  ga.n_rows = out->n_rows;
+  ga.rows_cap = c.rows_cap;
+  ga.d = d;
+  ga.x_perm = out->x_perm;
+  return cuda_status(launch_gather(ga, sms, stream));
 }
 
 int lynx_moe_forward(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
@@ -495,63 +537,11 @@ int lynx_moe_forward(const lynx_layer_t* layer, const uint16_t* hidden, int T, c
   return moe_forward_common(layer, hidden, T, assigned, weights, out, nullptr, workspace, workspace_bytes, stream);
 }
 
-/* Same as lynx_moe_forward, but writes the f32 expert sum WITHOUT the
- * residual (expert-parallel partial; assigned entries < 0 are skipped). */
 int lynx_moe_forward_partial(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
                              const double* weights, float* partial_out, void* workspace, size_t workspace_bytes,
                              lynx_stream_t stream) {
   return moe_forward_common(layer, hidden, T, assigned, weights, nullptr, partial_out, workspace, workspace_bytes,
                             stream);
-}
-
-static int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode,
-                          const lynx_policy_t* policy, uint16_t* out, const lynx_selection_t* sel, void* workspace,
-                          size_t workspace_bytes, lynx_stream_t stream, cudaEvent_t const* ev) {
-  int st = check_layer(layer, T);
-  if (st) return st;
-  if (!layer->router_wt) return LYNX_ERR_SHAPE;
-  const int N = layer->num_experts, k = layer->top_k;
-  int floor_keep = k;
-  st = check_policy(policy, N, k, decode, &floor_keep);
-  if (st) return st;
-  const Plan P = plan_for(layer, T, true);
-  if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
-  void* ws = aligned_ws(workspace);
-
-  double* logits = at<double>(ws, P.logits);
-  if (ev) cudaEventRecord(ev[0], stream);
-  st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, logits, stream));
-  if (st) return st;
-
-  SelectArgs a;
-  a.logits = logits;
-  a.T = T;
-  a.N = N;
-  a.k = k;
-  a.decode = decode;
-  if (policy) {
-    a.pol = *policy;
-  } else {
-    a.pol = lynx_policy_t{};
-    a.pol.mode = LYNX_POLICY_NONE;
-  }
-  a.floor_keep = floor_keep;
-#define LYNX_PICK(field, off, type) ((sel && sel->field) ? sel->field : at<type>(ws, P.off))
-  a.ids = LYNX_PICK(expert_ids, ids, int32_t);
-  a.probs = LYNX_PICK(probs, probs, double);
-  a.full = LYNX_PICK(full_probs, full, double);
-  a.conf = LYNX_PICK(conf, conf, double);
-  a.counts = LYNX_PICK(counts, counts, double);
-  a.retained = LYNX_PICK(retained, retained, uint8_t);
-  a.assigned = LYNX_PICK(assigned, assigned, int32_t);
-  a.weights = LYNX_PICK(weights, weights, double);
-  a.important = LYNX_PICK(important, important, uint8_t);
-  a.flags = LYNX_PICK(flags, flags, int32_t);
-#undef LYNX_PICK
-  if (ev) cudaEventRecord(ev[1], stream);
-  st = cuda_status(launch_route_select(a, stream));
-  if (st) return st;
-  return forward_impl(layer, hidden, T, a.assigned, a.weights, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr);
 }
 
 int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,

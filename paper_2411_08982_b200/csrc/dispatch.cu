@@ -1,6 +1,5 @@
-// dispatch.cu -- K2 histogram/scan permutation + gather, K4 weighted
-// combine, gate/up weight packing and the expert-parallel pack/combine
-// helpers.
+// dispatch.cu -- K2 gather of the dispatched rows, gate/up weight packing
+// and the expert-parallel pack/combine helpers.
 //
 // Reference order (simulator.py:101-113): out = hidden.copy(); for each
 // used expert e ascending (np.unique(assigned)), rows = the tokens with a
@@ -13,197 +12,31 @@
 
 namespace lynx {
 
-constexpr int kPermThreads = 512;
-
-__device__ __forceinline__ int round16(int v) { return (v + 15) & ~15; }
-
-// Every CTA rebuilds the (tiny) expert x token bitmap in shared memory, so
-// no grid-wide barrier is needed; CTAs then split the tokens for the
-// gather and the per-token bookkeeping.
-__global__ void __launch_bounds__(kPermThreads) permute_kernel(PermuteArgs a) {
-  extern __shared__ uint32_t s_bits[];  // [N][W] bitmap, then [N][W] prefix counts
-  __shared__ int s_cnt[LYNX_MAX_EXPERTS];
-  __shared__ int s_base[LYNX_MAX_EXPERTS];
-  __shared__ int s_list_row[LYNX_MAX_TOPK];
-  __shared__ float s_list_w[LYNX_MAX_TOPK];
-  __shared__ int s_nl;
-
-  const int T = a.T, N = a.N, k = a.k, d = a.d;
-  const int W = (T + 31) >> 5;
-  int* s_prefix = reinterpret_cast<int*>(s_bits + N * W);
-  const int tid = threadIdx.x;
-
-  for (int i = tid; i < N * W; i += blockDim.x) s_bits[i] = 0;
-  __syncthreads();
-  for (int i = tid; i < T * k; i += blockDim.x) {
-    const int e = a.assigned[i];
-    if (e >= 0 && e < N) {
-      const int t = i / k;
-      atomicOr(&s_bits[e * W + (t >> 5)], 1u << (t & 31));
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < N; e += blockDim.x) {
-    int run = 0;
-    for (int w = 0; w < W; ++w) {
-      s_prefix[e * W + w] = run;
-      run += __popc(s_bits[e * W + w]);
-    }
-    s_cnt[e] = run;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int base = 0, nseg = 0, nused = 0;
-    for (int e = 0; e < N; ++e) {
-      const int cnt = s_cnt[e];
-      if (cnt == 0) {
-        s_base[e] = -1;
-        continue;
-      }
-      s_base[e] = base;
-      ++nused;
-      for (int c0 = 0; c0 < cnt; c0 += LYNX_SEG_ROWS) {
-        if (blockIdx.x == 0) {
-          a.out.seg_expert[nseg] = e;
-          a.out.seg_row[nseg] = base + c0;
-          a.out.seg_count[nseg] = cnt - c0 < LYNX_SEG_ROWS ? cnt - c0 : LYNX_SEG_ROWS;
-        }
-        ++nseg;
-      }
-      base += round16(cnt);
-    }
-    if (blockIdx.x == 0) {
-      *a.out.n_seg = nseg;
-      *a.out.n_used = nused;
-    }
-  }
-  if (blockIdx.x == 0)
-    for (int i = tid; i < a.n_counters; i += blockDim.x) a.counters[i] = 0;
-  __syncthreads();
-
-  const int nvec = d >> 3;  // 16-byte vectors per row
-  for (int t = blockIdx.x; t < T; t += gridDim.x) {
-    if (tid == 0) {
-      int ids[LYNX_MAX_TOPK];
-      int n = 0;
-      for (int c = 0; c < k; ++c) {
-        const int e = a.assigned[t * k + c];
-        if (e < 0 || e >= N) continue;
-        bool dup = false;
-        for (int j = 0; j < n; ++j) dup |= ids[j] == e;
-        if (dup) continue;
-        int j = n++;
-        while (j > 0 && ids[j - 1] > e) {
-          ids[j] = ids[j - 1];
-          --j;
-        }
-        ids[j] = e;
-      }
-      for (int j = 0; j < n; ++j) {
-        const int e = ids[j];
-        const uint32_t word = s_bits[e * W + (t >> 5)];
-        const int pos = s_prefix[e * W + (t >> 5)] + __popc(word & ((1u << (t & 31)) - 1u));
-        const int row = s_base[e] + pos;
-        double w = 0.0;
-        for (int c = 0; c < k; ++c)
-          if (a.assigned[t * k + c] == e) w += a.weights[t * k + c];
-        s_list_row[j] = row;
-        s_list_w[j] = static_cast<float>(w);
-        a.out.tok_rows[t * k + j] = row;
-        a.out.tok_weight[t * k + j] = static_cast<float>(w);
-        a.out.perm_token[row] = t;
-        a.out.perm_weight[row] = static_cast<float>(w);
-      }
-      for (int j = n; j < k; ++j) {
-        a.out.tok_rows[t * k + j] = -1;
-        a.out.tok_weight[t * k + j] = 0.f;
-      }
-      s_nl = n;
-    }
-    __syncthreads();
-    const uint4* src = reinterpret_cast<const uint4*>(a.hidden + static_cast<size_t>(t) * d);
-    for (int j = 0; j < s_nl; ++j) {
-      uint4* dst = reinterpret_cast<uint4*>(a.out.x_perm + static_cast<size_t>(s_list_row[j]) * d);
-      for (int v = tid; v < nvec; v += blockDim.x) dst[v] = src[v];
-    }
-    __syncthreads();
-  }
-  // Padding rows of each used expert: zero input, no token.
-  for (int e = blockIdx.x; e < N; e += gridDim.x) {
-    const int cnt = s_cnt[e];
-    if (cnt == 0) continue;
-    const int r0 = s_base[e] + cnt, r1 = s_base[e] + round16(cnt);
-    for (int r = r0; r < r1; ++r) {
-      uint4* dst = reinterpret_cast<uint4*>(a.out.x_perm + static_cast<size_t>(r) * d);
-      for (int v = tid; v < nvec; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
-      if (tid == 0) {
-        a.out.perm_token[r] = -1;
-        a.out.perm_weight[r] = 0.f;
-      }
-    }
+// K2: gather the dispatched token rows into the permuted buffer (expert
+// segments, 16-row padded) that K3's TMA tensor map covers.  One 16-byte
+// vector per thread; padding rows are zero.  The permutation itself was
+// planned by K1 (plan_dispatch in select.cu).
+__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int rows = *a.n_rows;
+  const int nvec = a.d >> 3;
+  const uint4* src = reinterpret_cast<const uint4*>(a.hidden);
+  uint4* dst = reinterpret_cast<uint4*>(a.x_perm);
+  const int total = rows * nvec;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int r = i / nvec, v = i - r * nvec;
+    const int t = a.perm_token[r];
+    dst[i] = t >= 0 ? src[static_cast<size_t>(t) * nvec + v] : make_uint4(0, 0, 0, 0);
   }
 }
 
-cudaError_t launch_permute(const PermuteArgs& a, int sm_count, cudaStream_t s) {
-  const int W = (a.T + 31) / 32;
-  const size_t smem = static_cast<size_t>(a.N) * W * 8;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  int grid = a.T < sm_count ? a.T : sm_count;
+cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
+  const long total = static_cast<long>(a.rows_cap) * (a.d >> 3);
+  long grid = (total + 255) / 256;
+  if (grid > 4L * sm_count) grid = 4L * sm_count;
   if (grid < 1) grid = 1;
-  permute_kernel<<<grid, kPermThreads, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------- K4
-// y[t] = hidden[t] + sum_j w_j * (sum_s partial[s][row_j]), j over the
-// token's experts ascending -- the reference's accumulation order.
-__global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
-  const int t = blockIdx.x;
-  const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
-  if (c >= a.d) return;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (a.hidden) {
-    const __nv_bfloat162* h =
-        reinterpret_cast<const __nv_bfloat162*>(a.hidden + static_cast<size_t>(t) * a.d + c);
-    const float2 h0 = __bfloat1622float2(h[0]), h1 = __bfloat1622float2(h[1]);
-    acc = make_float4(h0.x, h0.y, h1.x, h1.y);
-  }
-  for (int j = 0; j < a.k; ++j) {
-    const int row = a.tok_rows[t * a.k + j];
-    if (row < 0) break;
-    const float w = a.tok_weight[t * a.k + j];
-    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp = 0; sp < a.split2; ++sp) {
-      const float4 v = *reinterpret_cast<const float4*>(
-          a.partial + (static_cast<size_t>(sp) * a.rows_cap + row) * a.d + c);
-      y.x += v.x;
-      y.y += v.y;
-      y.z += v.z;
-      y.w += v.w;
-    }
-    acc.x += w * y.x;
-    acc.y += w * y.y;
-    acc.z += w * y.z;
-    acc.w += w * y.w;
-  }
-  const size_t o = static_cast<size_t>(t) * a.d + c;
-  if (a.out_f32) {
-    *reinterpret_cast<float4*>(a.out_f32 + o) = acc;
-  } else {
-    __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(a.out_bf16 + o);
-    out[0] = __floats2bfloat162_rn(acc.x, acc.y);
-    out[1] = __floats2bfloat162_rn(acc.z, acc.w);
-  }
-}
-
-cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s) {
-  dim3 grid(a.T, (a.d + 1023) / 1024);
-  combine_kernel<<<grid, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(gather_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, s, a);
 }
 
 // --------------------------------------------------------------- packing

@@ -12,8 +12,12 @@
 //        epilogue h = silu(gate) * up -> H[seg rows, 64 features] (bf16).
 //        TANH2:  epilogue h = tanh(acc) -> H[seg rows, 128 features].
 //   phase-1 unit (seg, mt, s):    D[128 x n] = W2[e][mt*128 : +128, K_s] . H_seg[:, K_s]^T
-//        epilogue -> partial[s][seg rows][mt*128 : +128] (f32), summed in a
-//        fixed order by K4 (deterministic, no float atomics).
+//        epilogue: Y[seg rows][mt*128 : +128] (f32) = D for s = 0, else
+//        Y += D after split s-1 has published -- a fixed summation order,
+//        so results are bit-reproducible without float atomics.  When the
+//        last split of the last segment of an m-tile lands, that warp
+//        applies the combine (simulator.py:101-112) for its 32 columns:
+//        out[t] = hidden[t] + sum_j w_tj * Y[row_tj], experts ascending.
 //
 // Swap-AB: weight rows are the MMA M (=128) dimension, the segment's tokens
 // the MMA N dimension (16..256, rounded to 16), so decode streams each used
@@ -75,6 +79,44 @@ __device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u,
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.f + __expf(-g)) * u; }
 
+// Combine for one output column r (all tokens): residual + experts in
+// ascending order, the reference's accumulation order (simulator.py:101-112).
+__device__ __noinline__ void combine_column(const FfnParams& p, int r) {
+  const float* Y = p.partial + r;
+  for (int t0 = 0; t0 < p.T; t0 += 4) {
+    float acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u;
+      acc[u] = 0.f;
+      if (t < p.T && p.hidden)
+        acc[u] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.hidden)[static_cast<size_t>(t) * p.d + r]);
+    }
+    for (int j = 0; j < p.k; ++j) {
+      float y[4], w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u;
+        const int row = t < p.T ? p.tok_rows[t * p.k + j] : -1;
+        w[u] = row >= 0 ? p.tok_weight[t * p.k + j] : 0.f;
+        y[u] = row >= 0 ? __ldcg(Y + static_cast<size_t>(row) * p.d) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += w[u] * y[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u;
+      if (t >= p.T) break;
+      const size_t o = static_cast<size_t>(t) * p.d + r;
+      if (p.out_f32)
+        p.out_f32[o] = acc[u];
+      else
+        reinterpret_cast<__nv_bfloat16*>(p.out_bf16)[o] = __float2bfloat16_rn(acc[u]);
+    }
+  }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_constant__ FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -118,9 +160,18 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Everything above overlapped the previous kernel (programmatic launch);
+  // the dispatch plan and gathered rows are only read after this point.
+  griddep_wait();
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
   const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
+  if (nseg == 0) {
+    // No token routed here (an expert-parallel shard can receive none):
+    // the output is the residual (or zeros for a partial).
+    if (warp >= 4)
+      for (int r = blockIdx.x * 128 + (threadIdx.x - 128); r < p.d; r += gridDim.x * 128) combine_column(p, r);
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -260,35 +311,62 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           }
         }
       } else {
-        const int r = U.mt * 128 + q * 32 + lane;
-        float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
+        // ---- phase 1: chained split-K accumulation into Y, then combine
+        const int r = U.mt * 128 + q * 32 + lane;  // output column (d index)
+        const bool rv = r < p.d;
+        float* Y = p.partial + static_cast<size_t>(U.row0) * p.d + r;
+        int* chain = p.counters + 1 + p.max_seg + U.seg * p.tiles2 + U.mt;
+        if (U.split > 0) {
+          Watchdog wd;
+          while (ld_acquire_gpu(chain) < 4 * U.split) wd.tick(9);
+        }
         for (int c0 = 0; c0 < U.nmma; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(tb + c0, v);
           tmem_ld_wait();
+          float prev[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int tok = c0 + j;
-            if (tok < U.n && r < p.d) dst[static_cast<size_t>(tok) * p.d] = __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j)
+            prev[j] = (U.split > 0 && c0 + j < U.n && rv) ? __ldcg(Y + static_cast<size_t>(c0 + j) * p.d) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < U.n && rv) __stcg(Y + static_cast<size_t>(c0 + j) * p.d, prev[j] + __uint_as_float(v[j]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) red_release_gpu_add(chain, 1);
+        if (U.split == p.split2 - 1) {
+          int* done = p.counters + 1 + p.max_seg + p.max_seg * p.tiles2 + U.mt * 4 + q;
+          int last = 0;
+          if (lane == 0) last = atom_add_acq_rel_gpu(done, 1) == nseg - 1;
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last && rv) {
+            fence_acq_rel_gpu();
+            combine_column(p, r);
           }
         }
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+        continue;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (U.phase == 0) {
-        // publish this warp's slice of H to phase-1 consumers on other SMs
-        __threadfence();
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
-      }
+      // publish this warp's slice of H to phase-1 consumers on other SMs
+      __threadfence();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
   }
   tc_fence_before();
   __syncthreads();
+  griddep_launch_dependents();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
@@ -309,8 +387,7 @@ static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s
     if (e != cudaSuccess) return e;
     configured_device = dev;
   }
-  ffn_kernel<BN, STAGES><<<sm_count, kFfnThreads, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(ffn_kernel<BN, STAGES>, dim3(sm_count), dim3(kFfnThreads), smem, s, p);
 }
 
 cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s) {

@@ -1,22 +1,71 @@
-// lynx_internal.cuh -- kernel argument structs and launchers shared by the
-// translation units behind the C ABI (include/lynx_b200.h).
+// lynx_internal.cuh -- kernel argument structs, programmatic-dependent-launch
+// helpers and launchers shared by the translation units behind the C ABI
+// (include/lynx_b200.h).
 #pragma once
 
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/lynx_b200.h"
 
 namespace lynx {
 
 constexpr int kSelectThreads = 512;
+constexpr size_t kSelectMaxSmem = 200 * 1024;
+
+// ------------------------------------------------- programmatic dependent launch
+// Every kernel of the layer chain is launched with programmatic stream
+// serialization: it may start while its predecessor drains, runs its
+// prologue, and calls griddep_wait() before touching anything the
+// predecessor (or anything before it) wrote.  Because every kernel waits
+// before it completes, completion stays transitive along the stream.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// Dispatch plan written by K1 (or the standalone plan kernel).
+struct PlanOut {
+  int enabled;
+  int32_t* n_seg;
+  int32_t* n_used;
+  int32_t* n_rows;      // rows of the permuted buffer in use (16-padded per expert)
+  int32_t* seg_expert;
+  int32_t* seg_row;
+  int32_t* seg_count;
+  int32_t* perm_token;  // [rows_cap] source token, -1 = padding
+  float* perm_weight;
+  int32_t* tok_rows;    // [T,k] permuted rows per token, experts ascending, -1 padded
+  float* tok_weight;
+  int* counters;        // FFN scheduler words zeroed for the next K3 launch
+  int n_counters;
+};
 
 struct SelectArgs {
-  const double* logits;
+  const double* logits;  // null: the selection (ids/probs/full) is an input
   int T, N, k, decode;
   lynx_policy_t pol;
   int floor_keep;  // resolved min_experts (>= k)
+  int stage;       // stage per-token arrays in shared memory
   int32_t* ids;
   double* probs;
   double* full;
@@ -27,35 +76,13 @@ struct SelectArgs {
   double* weights;
   uint8_t* important;
   int32_t* flags;
+  PlanOut plan;
 };
 
-// Dispatch bookkeeping the FFN and combine kernels read.
-struct DispatchView {
-  int32_t* n_seg;
-  int32_t* n_used;
-  int32_t* seg_expert;
-  int32_t* seg_row;
-  int32_t* seg_count;
-  int32_t* perm_token;
-  float* perm_weight;
-  int32_t* tok_rows;
-  float* tok_weight;
-  uint16_t* x_perm;
-};
-
-struct PermuteArgs {
-  const int32_t* assigned;
-  const double* weights;
-  const uint16_t* hidden;
-  int T, N, k, d;
-  int max_seg, rows_cap;
-  DispatchView out;
-  int* counters;   // FFN scheduler words to zero (may be null)
-  int n_counters;
-};
-
-// Grouped expert FFN (K3).  Phase 0 = gate/up (or tanh w1) over d,
-// phase 1 = down projection over ff, split-K into `split2` partials.
+// Grouped expert FFN (K3).  Phase 0 = gate/up (or tanh w1) over d, phase 1 =
+// down projection over ff, split-K into `split2` partials; the last phase-1
+// unit of every 128-column m-tile reduces the partials and applies the
+// combine (+ residual) for that tile.
 struct FfnParams {
   CUtensorMap map_w1;  // (d, rows1, E)   box (64, 128, 1)
   CUtensorMap map_w2;  // (ff, d, E)      box (64, 128, 1)
@@ -67,34 +94,43 @@ struct FfnParams {
   const int32_t* seg_count;
   uint16_t* h;      // [rows_cap, ff] bf16
   float* partial;   // [split2, rows_cap, d] f32
-  int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s
+  int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s,
+                    // [1 + max_seg + mt] phase-1 units done for m-tile mt
+  int max_seg;
   int d, ff, act;
   int tiles1, kb1;  // phase 0: 128-row tiles per segment, 64-wide k blocks
   int tiles2, split2, kb2_per, kb2_total;
   int rows_cap;
-};
-
-struct CombineArgs {
-  const uint16_t* hidden;  // residual (null -> no residual)
-  const float* partial;
-  int split2, rows_cap, T, k, d;
+  // fused combine (K4)
+  int T, k;
+  const uint16_t* hidden;   // residual; null -> no residual (EP partial)
   const int32_t* tok_rows;
   const float* tok_weight;
-  uint16_t* out_bf16;  // one of these is set
+  uint16_t* out_bf16;
   float* out_f32;
+};
+
+struct GatherArgs {
+  const uint16_t* hidden;
+  const int32_t* perm_token;
+  const int32_t* n_rows;
+  int rows_cap, d;
+  uint16_t* x_perm;
 };
 
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s);
+size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan);
+bool select_can_stage(int T, int N, int k, bool plan);
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s);
+cudaError_t launch_plan(const int32_t* asg, const double* w, int T, int N, int k, const PlanOut& o, cudaStream_t s);
 cudaError_t launch_remap(const int32_t* ids, const double* full, int T, int N, int k, const uint8_t* retained,
                          int32_t* assigned, double* weights, int32_t* flags, cudaStream_t s);
 cudaError_t launch_topk(const double* vals, int T, int N, int k, int32_t* ids, double* out, cudaStream_t s);
 cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_policy_t& w, double* counts,
                         cudaStream_t s);
-cudaError_t launch_permute(const PermuteArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s);
-cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s);
 cudaError_t launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,
                             cudaStream_t s);
 cudaError_t launch_ep_pack(const uint16_t* hidden_local, const int32_t* assigned, int T_local, int k, int N, int G,

@@ -1,6 +1,7 @@
-// select.cu -- K0 router GEMV (+RMSNorm) and K1 fused route + retention
-// policy + remap.  Decisions are bit-exact with the reference's float64
-// numpy path (see oracle/lynx_oracle.py for the restated algorithm).
+// select.cu -- K0 router GEMV (+RMSNorm), K1 fused route + retention policy
+// + remap + dispatch plan, and the small kernels behind the modular API.
+// Decisions are bit-exact with the reference's float64 numpy path (see
+// oracle/lynx_oracle.py for the restated algorithm).
 //
 // Reference:
 //   rms_norm / router_logits   simulator.py:26-27, 82-83
@@ -14,6 +15,11 @@
 //   latency_policy             policy.py:232-264
 //   select_important_tokens    policy.py:267-284
 //   accuracy_policy            policy.py:287-338
+//   dispatch order             simulator.py:104-112
+//
+// Latency, not bandwidth, bounds these kernels (a decode batch is a few KB
+// of routing state), so K1 is one CTA that stages every per-token array in
+// shared memory and never chains dependent global loads.
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -47,6 +53,8 @@ __device__ double np_pairwise_sum(const double* a, int n) {
   half -= half % 8;
   return np_pairwise_sum(a, half) + np_pairwise_sum(a + half, n - half);
 }
+
+__device__ __forceinline__ uint64_t expert_mask_all(int N) { return N == 64 ? ~0ull : ((1ull << N) - 1); }
 
 // Best expert in `cand` by (probability desc, index asc); -1 if none.
 __device__ __forceinline__ int best_of(const double* p, uint64_t cand, int N) {
@@ -89,185 +97,336 @@ __device__ __forceinline__ void remap_one(const int32_t* ids, const double* p, i
   for (int r = 0; r < k; ++r) weights[r] = slot_p[r] / total;
 }
 
+// ------------------------------------------------------------- dispatch plan
+// forward_layer's grouping (simulator.py:104-112): used experts ascending,
+// each expert's token rows ascending, a token's duplicate slots on one expert
+// merged (weights summed in slot order).  Rows of expert e occupy
+// [base[e], base[e] + cnt[e]) in the permuted buffer, base 16-aligned;
+// segments split an expert at LYNX_SEG_ROWS rows.  Called by every thread of
+// one CTA; `asg`/`w` may live in shared or global memory.
+__device__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N, int k, const PlanOut& o,
+                              uint32_t* s_bits, int* s_prefix) {
+  __shared__ int s_cnt[LYNX_MAX_EXPERTS];
+  __shared__ int s_base[LYNX_MAX_EXPERTS];
+  const int W = (T + 31) >> 5;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < N * W; i += nthr) s_bits[i] = 0;
+  __syncthreads();
+  for (int i = tid; i < T * k; i += nthr) {
+    const int e = asg[i];
+    if (e >= 0 && e < N) {
+      const int t = i / k;
+      atomicOr(&s_bits[e * W + (t >> 5)], 1u << (t & 31));
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < N; e += nthr) {
+    int run = 0;
+    for (int q = 0; q < W; ++q) {
+      s_prefix[e * W + q] = run;
+      run += __popc(s_bits[e * W + q]);
+    }
+    s_cnt[e] = run;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int base = 0, nseg = 0, nused = 0;
+    for (int e = 0; e < N; ++e) {
+      const int cnt = s_cnt[e];
+      s_base[e] = base;
+      if (cnt == 0) continue;
+      ++nused;
+      for (int c0 = 0; c0 < cnt; c0 += LYNX_SEG_ROWS) {
+        o.seg_expert[nseg] = e;
+        o.seg_row[nseg] = base + c0;
+        o.seg_count[nseg] = min(LYNX_SEG_ROWS, cnt - c0);
+        ++nseg;
+      }
+      base += (cnt + 15) & ~15;
+    }
+    *o.n_seg = nseg;
+    *o.n_used = nused;
+    *o.n_rows = base;
+  }
+  for (int i = tid; i < o.n_counters; i += nthr) o.counters[i] = 0;
+  __syncthreads();
+  for (int t = tid; t < T; t += nthr) {
+    int ids[LYNX_MAX_TOPK];
+    int n = 0;
+    for (int c = 0; c < k; ++c) {
+      const int e = asg[t * k + c];
+      if (e < 0 || e >= N) continue;
+      bool dup = false;
+      for (int j = 0; j < n; ++j) dup |= ids[j] == e;
+      if (dup) continue;
+      int j = n++;
+      while (j > 0 && ids[j - 1] > e) {
+        ids[j] = ids[j - 1];
+        --j;
+      }
+      ids[j] = e;
+    }
+    for (int j = 0; j < n; ++j) {
+      const int e = ids[j];
+      const uint32_t word = s_bits[e * W + (t >> 5)];
+      const int row = s_base[e] + s_prefix[e * W + (t >> 5)] + __popc(word & ((1u << (t & 31)) - 1u));
+      double acc = 0.0;
+      for (int c = 0; c < k; ++c)
+        if (asg[t * k + c] == e) acc += w[t * k + c];
+      const float wf = static_cast<float>(acc);
+      o.tok_rows[t * k + j] = row;
+      o.tok_weight[t * k + j] = wf;
+      o.perm_token[row] = t;
+      o.perm_weight[row] = wf;
+    }
+    for (int j = n; j < k; ++j) {
+      o.tok_rows[t * k + j] = -1;
+      o.tok_weight[t * k + j] = 0.f;
+    }
+  }
+  for (int e = tid; e < N; e += nthr) {
+    const int cnt = s_cnt[e];
+    for (int r = s_base[e] + cnt; r < s_base[e] + ((cnt + 15) & ~15); ++r) {
+      o.perm_token[r] = -1;
+      o.perm_weight[r] = 0.f;
+    }
+  }
+}
+
+// Shared-memory carve-up of K1 (host computes the same with select_smem_bytes).
+struct SelectSmem {
+  size_t p, conf, ids, probs, asg, w, imp, bits, prefix, total;
+};
+
+__host__ __device__ inline SelectSmem select_smem(int T, int N, int k, bool stage, bool plan) {
+  SelectSmem s{};
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    const size_t o = off;
+    off = (off + b + 15) & ~size_t(15);
+    return o;
+  };
+  if (stage) {
+    s.p = take(sizeof(double) * T * N);
+    s.conf = take(sizeof(double) * T);
+    s.ids = take(sizeof(int32_t) * T * k);
+    s.probs = take(sizeof(double) * T * k);
+    s.asg = take(sizeof(int32_t) * T * k);
+    s.w = take(sizeof(double) * T * k);
+  }
+  s.imp = take(T);
+  if (plan) {
+    const int W = (T + 31) >> 5;
+    s.bits = take(sizeof(uint32_t) * N * W);
+    s.prefix = take(sizeof(int) * N * W);
+  }
+  s.total = off;
+  return s;
+}
+
 // ------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs a) {
   __shared__ double s_counts[LYNX_MAX_EXPERTS];
+  __shared__ int s_icount[LYNX_MAX_EXPERTS];
   __shared__ int s_rank[LYNX_MAX_EXPERTS];
   __shared__ int s_order[LYNX_MAX_EXPERTS];
   __shared__ int s_keep[LYNX_MAX_EXPERTS];
   __shared__ int s_flags, s_nq, s_clipped;
   __shared__ unsigned long long s_keepmask;
-  extern __shared__ uint8_t s_imp[];  // [T]
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+
+  griddep_launch_dependents();
+  griddep_wait();  // logits come from K0 (programmatic dependent launch)
 
   const int T = a.T, N = a.N, k = a.k;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const SelectSmem L = select_smem(T, N, k, a.stage, a.plan.enabled);
+  // Working arrays: shared memory when they fit, else the caller's outputs.
+  double* P = a.stage ? reinterpret_cast<double*>(s_dyn + L.p) : a.full;
+  double* CONF = a.stage ? reinterpret_cast<double*>(s_dyn + L.conf) : a.conf;
+  int32_t* IDS = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.ids) : a.ids;
+  double* PROBS = a.stage ? reinterpret_cast<double*>(s_dyn + L.probs) : a.probs;
+  int32_t* ASG = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.asg) : a.assigned;
+  double* WT = a.stage ? reinterpret_cast<double*>(s_dyn + L.w) : a.weights;
+  uint8_t* IMP = s_dyn + L.imp;
+
   if (tid == 0) {
     s_flags = 0;
     s_nq = 0;
     s_clipped = 0;
   }
+  for (int e = tid; e < N; e += nthr) s_icount[e] = 0;
+  if (!a.logits && a.stage) {  // apply_policy on a given selection: stage it
+    for (int i = tid; i < T * N; i += nthr) P[i] = a.full[i];
+    for (int i = tid; i < T * k; i += nthr) {
+      IDS[i] = a.ids[i];
+      PROBS[i] = a.probs[i];
+    }
+  }
   __syncthreads();
 
-  // 1) softmax + top-k (when routing from logits) + confidence, one thread
-  //    per token.  With logits == null the selection (ids/probs/full) is an
-  //    input: apply_policy on an existing ExpertSelection.
-  for (int t = tid; t < T; t += blockDim.x) {
-    double* p = a.full + static_cast<size_t>(t) * N;
+  // 1) softmax + top-k (when routing from logits) + confidence, thread per token.
+  for (int t = tid; t < T; t += nthr) {
+    double* p = P + static_cast<size_t>(t) * N;
     if (a.logits) {
       const double* z = a.logits + static_cast<size_t>(t) * N;
-      double m = z[0];
+#pragma unroll 8
+      for (int i = 0; i < N; ++i) p[i] = z[i];  // independent loads, staged
+      double m = p[0];
       bool finite = true;
       for (int i = 0; i < N; ++i) {
-        const double v = z[i];
+        const double v = p[i];
         finite &= isfinite(v);
         m = v > m ? v : m;
       }
       if (!finite) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
-      for (int i = 0; i < N; ++i) p[i] = exp(z[i] - m);
+      for (int i = 0; i < N; ++i) p[i] = exp(p[i] - m);
       const double s = np_pairwise_sum(p, N);
       for (int i = 0; i < N; ++i) p[i] = p[i] / s;
       uint64_t taken = 0;
       for (int r = 0; r < k; ++r) {
-        const int b = best_of(p, ~taken & (N == 64 ? ~0ull : ((1ull << N) - 1)), N);
+        const int b = best_of(p, expert_mask_all(N) & ~taken, N);
         taken |= 1ull << b;
-        a.ids[t * k + r] = b;
-        a.probs[t * k + r] = p[b];
+        IDS[t * k + r] = b;
+        PROBS[t * k + r] = p[b];
       }
     }
     double top1 = p[0];
-    for (int i = 1; i < N; ++i) top1 = p[i] > top1 ? p[i] : top1;
+    int first = 0;
+    for (int i = 1; i < N; ++i)
+      if (p[i] > top1) {
+        top1 = p[i];
+        first = i;
+      }
     double c = top1;
     if (a.pol.confidence_metric == LYNX_CONF_MARGIN) {
       if (N == 1) {
         c = p[0];
-      } else {
-        // np.sort(full)[-1] - np.sort(full)[-2]: the two largest values
-        int first = 0;
-        for (int i = 1; i < N; ++i)
-          if (p[i] > p[first]) first = i;
+      } else {  // np.sort(full)[-1] - np.sort(full)[-2]
         double second = -1.0;
         for (int i = 0; i < N; ++i)
           if (i != first && p[i] > second) second = p[i];
         c = top1 - second;
       }
     }
-    a.conf[t] = c;
+    CONF[t] = c;
   }
   __syncthreads();
 
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
+  const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
   if (!run_policy) {
     // full_retain_mask: identity, weights = probs / row sum.
-    for (int t = tid; t < T; t += blockDim.x) {
-      const double s = np_pairwise_sum(a.probs + t * k, k);
+    for (int t = tid; t < T; t += nthr) {
+      const double s = np_pairwise_sum(PROBS + t * k, k);
       for (int r = 0; r < k; ++r) {
-        a.assigned[t * k + r] = a.ids[t * k + r];
-        a.weights[t * k + r] = a.probs[t * k + r] / s;
+        ASG[t * k + r] = IDS[t * k + r];
+        WT[t * k + r] = PROBS[t * k + r] / s;
       }
+      IMP[t] = 0;
     }
-    for (int e = tid; e < N; e += blockDim.x) {
-      if (a.retained) a.retained[e] = 1;
-      if (a.counts) a.counts[e] = 0.0;
+    for (int e = tid; e < N; e += nthr) {
+      s_keep[e] = 1;
+      s_counts[e] = 0.0;
     }
-    for (int t = tid; t < T; t += blockDim.x)
-      if (a.important) a.important[t] = 0;
-    __syncthreads();
-    if (tid == 0) a.flags[0] = s_flags;
-    return;
-  }
-
-  const bool accuracy = a.pol.mode == LYNX_POLICY_ACCURACY;
-  // 2a) important tokens (accuracy) -- select_important_tokens.
-  if (accuracy) {
-    const double tau = a.pol.confidence_threshold;
-    int local = 0;
-    for (int t = tid; t < T; t += blockDim.x) {
-      const bool q = a.conf[t] >= tau;
-      s_imp[t] = q ? 1 : 0;
-      local += q;
-    }
-    if (local) atomicAdd(&s_nq, local);
-    __syncthreads();
-    const int nq = s_nq;
-    const int S = a.pol.sample_threshold;
-    if (nq == 0) {
-      if (tid == 0) {
-        int best = 0;
-        for (int t = 1; t < T; ++t)
-          if (a.conf[t] > a.conf[best]) best = t;
-        s_imp[best] = 1;
+  } else {
+    // 2a) important tokens (accuracy) -- select_important_tokens.
+    if (accuracy) {
+      const double tau = a.pol.confidence_threshold;
+      int local = 0;
+      for (int t = tid; t < T; t += nthr) {
+        const bool q = CONF[t] >= tau;
+        IMP[t] = q ? 1 : 0;
+        local += q;
       }
-    } else if (nq > S) {
-      // keep the S most confident qualifying tokens (conf desc, t asc);
-      // ranks come from conf alone, so marking drops in bit 1 is race-free.
-      for (int t = tid; t < T; t += blockDim.x) {
-        if (!s_imp[t]) continue;
-        const double ct = a.conf[t];
-        int rank = 0;
-        for (int u = 0; u < T; ++u) {
-          const double cu = a.conf[u];
-          if (cu >= tau && (cu > ct || (cu == ct && u < t))) ++rank;
+      if (local) atomicAdd(&s_nq, local);
+      __syncthreads();
+      const int nq = s_nq;
+      const int S = a.pol.sample_threshold;
+      if (nq == 0) {
+        if (tid == 0) {
+          int best = 0;
+          for (int t = 1; t < T; ++t)
+            if (CONF[t] > CONF[best]) best = t;
+          IMP[best] = 1;
         }
-        if (rank >= S) s_imp[t] |= 2;
+      } else if (nq > S) {
+        // keep the S most confident qualifying tokens (conf desc, t asc);
+        // ranks come from CONF alone, so marking drops in bit 1 is race-free.
+        for (int t = tid; t < T; t += nthr) {
+          if (!IMP[t]) continue;
+          const double ct = CONF[t];
+          int rank = 0;
+          for (int u = 0; u < T; ++u) {
+            const double cu = CONF[u];
+            rank += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
+          }
+          if (rank >= S) IMP[t] |= 2;
+        }
+        __syncthreads();
+        for (int t = tid; t < T; t += nthr) IMP[t] = IMP[t] == 1;
       }
       __syncthreads();
-      for (int t = tid; t < T; t += blockDim.x) s_imp[t] = s_imp[t] == 1;
     }
-    __syncthreads();
-  }
-
-  // 2b) vote tally (over all tokens, or the important ones), slot order.
-  for (int e = tid; e < N; e += blockDim.x) {
-    double c = 0.0;
-    for (int t = 0; t < T; ++t) {
-      if (accuracy && !s_imp[t]) continue;
-      for (int r = 0; r < k; ++r)
-        if (a.ids[t * k + r] == e) c += a.pol.n_rank_weights ? a.pol.rank_weights[r] : 1.0;
-    }
-    s_counts[e] = c;
-  }
-  __syncthreads();
-  // 2c) retention order: count desc, index asc.
-  for (int e = tid; e < N; e += blockDim.x) {
-    const double ce = s_counts[e];
-    int rank = 0;
-    for (int f = 0; f < N; ++f) {
-      const double cf = s_counts[f];
-      if (cf > ce || (cf == ce && f < e)) ++rank;
-    }
-    s_rank[e] = rank;
-    s_order[rank] = e;
-  }
-  __syncthreads();
-
-  const int floor_keep = a.floor_keep;
-  if (!accuracy) {
-    // latency_policy: drop the `eff` least-voted experts.
-    int eff = a.pol.drop_count;
-    const int room = N - floor_keep > 0 ? N - floor_keep : 0;
-    if (eff > room) eff = room;
-    for (int e = tid; e < N; e += blockDim.x) s_keep[e] = s_rank[e] < N - eff;
-    if (tid == 0) s_clipped = eff != a.pol.drop_count;
-  } else {
-    int budget = a.pol.freq_keep_budget < N ? a.pol.freq_keep_budget : N;
-    for (int e = tid; e < N; e += blockDim.x) s_keep[e] = (s_counts[e] > 0.0 && s_rank[e] < budget) ? 1 : 0;
-    __syncthreads();
-    for (int t = tid; t < T; t += blockDim.x)
-      if (s_imp[t]) s_keep[a.ids[t * k]] = 1;
-    __syncthreads();
-    if (tid == 0) {
-      int cnt = 0;
-      for (int e = 0; e < N; ++e) cnt += s_keep[e];
-      int padded = 0;
-      for (int pos = 0; pos < N && cnt < floor_keep; ++pos) {
-        const int e = s_order[pos];
-        if (!s_keep[e]) {
-          s_keep[e] = 1;
-          ++cnt;
-          padded = 1;
+    // 2b) vote tally over all (or the important) tokens.  Unit votes are
+    //     integers: order-free atomics are exact.  Rank-weighted votes are
+    //     float sums and keep numpy's slot order (one thread per expert).
+    if (!a.pol.n_rank_weights) {
+      for (int i = tid; i < T * k; i += nthr)
+        if (!accuracy || IMP[i / k]) atomicAdd(&s_icount[IDS[i]], 1);
+      __syncthreads();
+      for (int e = tid; e < N; e += nthr) s_counts[e] = static_cast<double>(s_icount[e]);
+    } else {
+      for (int e = tid; e < N; e += nthr) {
+        double c = 0.0;
+        for (int t = 0; t < T; ++t) {
+          if (accuracy && !IMP[t]) continue;
+          for (int r = 0; r < k; ++r)
+            if (IDS[t * k + r] == e) c += a.pol.rank_weights[r];
         }
+        s_counts[e] = c;
       }
-      s_clipped = padded;
+    }
+    __syncthreads();
+    // 2c) retention order: count desc, index asc.
+    for (int e = tid; e < N; e += nthr) {
+      const double ce = s_counts[e];
+      int rank = 0;
+      for (int f = 0; f < N; ++f) {
+        const double cf = s_counts[f];
+        rank += (cf > ce || (cf == ce && f < e)) ? 1 : 0;
+      }
+      s_rank[e] = rank;
+      s_order[rank] = e;
+    }
+    __syncthreads();
+    if (!accuracy) {
+      // latency_policy: drop the `eff` least-voted experts.
+      const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
+      const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
+      for (int e = tid; e < N; e += nthr) s_keep[e] = s_rank[e] < N - eff;
+      if (tid == 0) s_clipped = eff != a.pol.drop_count;
+    } else {
+      const int budget = a.pol.freq_keep_budget < N ? a.pol.freq_keep_budget : N;
+      for (int e = tid; e < N; e += nthr) s_keep[e] = (s_counts[e] > 0.0 && s_rank[e] < budget) ? 1 : 0;
+      __syncthreads();
+      for (int t = tid; t < T; t += nthr)
+        if (IMP[t]) s_keep[IDS[t * k]] = 1;
+      __syncthreads();
+      if (tid == 0) {
+        int cnt = 0;
+        for (int e = 0; e < N; ++e) cnt += s_keep[e];
+        int padded = 0;
+        for (int pos = 0; pos < N && cnt < a.floor_keep; ++pos) {
+          const int e = s_order[pos];
+          if (!s_keep[e]) {
+            s_keep[e] = 1;
+            ++cnt;
+            padded = 1;
+          }
+        }
+        s_clipped = padded;
+      }
     }
   }
   __syncthreads();
@@ -280,19 +439,51 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   __syncthreads();
 
   // 3) remap every token onto the retained set.
-  const uint64_t keep = s_keepmask;
-  for (int t = tid; t < T; t += blockDim.x)
-    remap_one(a.ids + t * k, a.full + static_cast<size_t>(t) * N, k, N, keep, a.assigned + t * k,
-              a.weights + t * k, &s_flags);
+  if (run_policy) {
+    const uint64_t keep = s_keepmask;
+    for (int t = tid; t < T; t += nthr)
+      remap_one(IDS + t * k, P + static_cast<size_t>(t) * N, k, N, keep, ASG + t * k, WT + t * k, &s_flags);
+  }
+  __syncthreads();
 
-  for (int e = tid; e < N; e += blockDim.x) {
+  // 4) outputs
+  if (a.stage) {
+    if (a.logits) {
+      for (int i = tid; i < T * N; i += nthr) a.full[i] = P[i];
+      for (int i = tid; i < T * k; i += nthr) {
+        a.ids[i] = IDS[i];
+        a.probs[i] = PROBS[i];
+      }
+    }
+    for (int t = tid; t < T; t += nthr) a.conf[t] = CONF[t];
+    for (int i = tid; i < T * k; i += nthr) {
+      a.assigned[i] = ASG[i];
+      a.weights[i] = WT[i];
+    }
+  }
+  for (int e = tid; e < N; e += nthr) {
     if (a.retained) a.retained[e] = static_cast<uint8_t>(s_keep[e]);
     if (a.counts) a.counts[e] = s_counts[e];
   }
-  for (int t = tid; t < T; t += blockDim.x)
-    if (a.important) a.important[t] = accuracy ? s_imp[t] : 0;
-  __syncthreads();
+  if (a.important)
+    for (int t = tid; t < T; t += nthr) a.important[t] = accuracy ? IMP[t] : 0;
   if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
+
+  // 5) dispatch plan for K2/K3 (layer path)
+  if (a.plan.enabled)
+    plan_dispatch(ASG, WT, T, N, k, a.plan, reinterpret_cast<uint32_t*>(s_dyn + L.bits),
+                  reinterpret_cast<int*>(s_dyn + L.prefix));
+}
+
+// Dispatch plan from an assigned/weights mask in global memory (forward_layer path).
+__global__ void __launch_bounds__(kSelectThreads) plan_kernel(const int32_t* asg, const double* w, int T, int N,
+                                                              int k, PlanOut o) {
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  griddep_launch_dependents();
+  griddep_wait();
+  const int W = (T + 31) >> 5;
+  plan_dispatch(asg, w, T, N, k, o, reinterpret_cast<uint32_t*>(s_dyn),
+                reinterpret_cast<int*>(s_dyn + sizeof(uint32_t) * N * W));
 }
 
 // remap_tokens on a caller-supplied retained mask.
@@ -315,22 +506,56 @@ __global__ void remap_kernel(const int32_t* ids, const double* full, int T, int 
   if (threadIdx.x == 0 && s_flags) atomicOr(flags, s_flags);
 }
 
+// top_k_select (router.py:157-171) over float64 rows: (value desc, index asc).
+__global__ void topk_kernel(const double* vals, int T, int N, int k, int32_t* ids, double* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const double* p = vals + static_cast<size_t>(t) * N;
+  uint64_t taken = 0;
+  for (int r = 0; r < k; ++r) {
+    const int b = best_of(p, expert_mask_all(N) & ~taken, N);
+    taken |= 1ull << b;
+    ids[t * k + r] = b;
+    out[t * k + r] = p[b];
+  }
+}
+
+// vote_expert_frequencies (policy.py:116-138): slots in row-major order.
+__global__ void vote_kernel(const int32_t* ids, int T, int k, int N, lynx_policy_t w, double* counts) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  double c = 0.0;
+  for (int t = 0; t < T; ++t)
+    for (int r = 0; r < k; ++r)
+      if (ids[t * k + r] == e) c += w.n_rank_weights ? w.rank_weights[r] : 1.0;
+  counts[e] = c;
+}
+
 // ------------------------------------------------------------------- K0
-// logits[t, n] = (h_t . Wr_n) / sqrt(mean(h_t^2) + 1e-12); one CTA per token,
-// 16-byte vector loads of the bf16 row and the [N, d] router weights.
-template <int NT>
+// logits[t, n] = (h_t . Wr_n) / sqrt(mean(h_t^2) + 1e-12).  One CTA per
+// (token, group of 8 experts); every thread issues its 1 + 8 independent
+// 16-byte loads before any math, so an iteration costs one memory latency.
 __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __restrict__ hidden,
                                                             const uint16_t* __restrict__ wt, int d, int N,
                                                             double* __restrict__ logits) {
+  griddep_launch_dependents();
   const int t = blockIdx.x;
+  const int n0 = blockIdx.y * 8;
   const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hidden) + static_cast<size_t>(t) * d;
   const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(wt);
-  float acc[NT];
+  float acc[8];
 #pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n] = 0.f;
+  for (int n = 0; n < 8; ++n) acc[n] = 0.f;
   float ss = 0.f;
+  griddep_wait();  // hidden may be produced by the previous kernel
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    uint4 wv[8];
     const uint4 hv = *reinterpret_cast<const uint4*>(h + c);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int e = min(n0 + n, N - 1);
+      wv[n] = __ldg(reinterpret_cast<const uint4*>(w + static_cast<size_t>(e) * d + c));
+    }
     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv);
     float hf[8];
 #pragma unroll
@@ -341,57 +566,80 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __re
       ss += f.x * f.x + f.y * f.y;
     }
 #pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      if (n < N) {
-        const uint4 wv = *reinterpret_cast<const uint4*>(w + static_cast<size_t>(n) * d + c);
-        const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv);
+    for (int n = 0; n < 8; ++n) {
+      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[n]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(w2[j]);
-          acc[n] += hf[2 * j] * f.x + hf[2 * j + 1] * f.y;
-        }
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(w2[j]);
+        acc[n] += hf[2 * j] * f.x + hf[2 * j + 1] * f.y;
       }
     }
   }
-  __shared__ float s_red[8][NT + 1];
+  __shared__ float s_red[8][9];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int n = 0; n <= NT; ++n) {
-    float v = n < NT ? acc[n] : ss;
+  for (int n = 0; n < 9; ++n) {
+    float v = n < 8 ? acc[n] : ss;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) s_red[warp][n] = v;
   }
   __syncthreads();
-  if (threadIdx.x <= NT) {
+  if (threadIdx.x < 9) {
     float v = 0.f;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) v += s_red[i][threadIdx.x];
+    for (int i = 0; i < 8; ++i) v += s_red[i][threadIdx.x];
     s_red[0][threadIdx.x] = v;
   }
   __syncthreads();
-  if (threadIdx.x < N) {
-    const double inv = 1.0 / sqrt(static_cast<double>(s_red[0][NT]) / d + 1e-12);
-    logits[static_cast<size_t>(t) * N + threadIdx.x] = static_cast<double>(s_red[0][threadIdx.x]) * inv;
+  if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
+    const double inv = 1.0 / sqrt(static_cast<double>(s_red[0][8]) / d + 1e-12);
+    logits[static_cast<size_t>(t) * N + n0 + threadIdx.x] = static_cast<double>(s_red[0][threadIdx.x]) * inv;
   }
 }
 
+// ------------------------------------------------------------- launchers
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s) {
-  if (N <= 8)
-    router_logits_kernel<8><<<T, 256, 0, s>>>(hidden, wt, d, N, logits);
-  else if (N <= 16)
-    router_logits_kernel<16><<<T, 256, 0, s>>>(hidden, wt, d, N, logits);
-  else if (N <= 32)
-    router_logits_kernel<32><<<T, 256, 0, s>>>(hidden, wt, d, N, logits);
-  else
-    router_logits_kernel<64><<<T, 256, 0, s>>>(hidden, wt, d, N, logits);
-  return cudaGetLastError();
+  return launch_pdl(router_logits_kernel, dim3(T, (N + 7) / 8), dim3(256), 0, s, hidden, wt, d, N, logits);
+}
+
+size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan) {
+  return select_smem(T, N, k, stage, plan).total;
+}
+
+bool select_can_stage(int T, int N, int k, bool plan) {
+  return select_smem(T, N, k, true, plan).total <= kSelectMaxSmem;
 }
 
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(a.T);
-  route_select_kernel<<<1, kSelectThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  const size_t smem = select_smem_bytes(a.T, a.N, a.k, a.stage, a.plan.enabled);
+  if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
+  static int configured_device = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_device != dev) {
+    cudaError_t e = cudaFuncSetAttribute(route_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSelectMaxSmem));
+    if (e != cudaSuccess) return e;
+    configured_device = dev;
+  }
+  return launch_pdl(route_select_kernel, dim3(1), dim3(kSelectThreads), smem, s, a);
+}
+
+cudaError_t launch_plan(const int32_t* asg, const double* w, int T, int N, int k, const PlanOut& o, cudaStream_t s) {
+  const int W = (T + 31) / 32;
+  const size_t smem = static_cast<size_t>(N) * W * 8;
+  if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
+  static int configured_device = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_device != dev) {
+    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSelectMaxSmem));
+    if (e != cudaSuccess) return e;
+    configured_device = dev;
+  }
+  return launch_pdl(plan_kernel, dim3(1), dim3(kSelectThreads), smem, s, asg, w, T, N, k, o);
 }
 
 cudaError_t launch_remap(const int32_t* ids, const double* full, int T, int N, int k, const uint8_t* retained,
@@ -399,38 +647,6 @@ cudaError_t launch_remap(const int32_t* ids, const double* full, int T, int N, i
   const int blocks = (T + 255) / 256;
   remap_kernel<<<blocks, 256, 0, s>>>(ids, full, T, N, k, retained, assigned, weights, flags);
   return cudaGetLastError();
-}
-
-}  // namespace lynx
-
-namespace lynx {
-
-// top_k_select (router.py:157-171) over arbitrary float64 rows:
-// k largest by (value desc, index asc).
-__global__ void topk_kernel(const double* vals, int T, int N, int k, int32_t* ids, double* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const double* p = vals + static_cast<size_t>(t) * N;
-  uint64_t taken = 0;
-  const uint64_t all = N == 64 ? ~0ull : ((1ull << N) - 1);
-  for (int r = 0; r < k; ++r) {
-    const int b = best_of(p, all & ~taken, N);
-    taken |= 1ull << b;
-    ids[t * k + r] = b;
-    out[t * k + r] = p[b];
-  }
-}
-
-// vote_expert_frequencies (policy.py:116-138): per expert, slots in
-// row-major order; optional per-rank weights.
-__global__ void vote_kernel(const int32_t* ids, int T, int k, int N, lynx_policy_t w, double* counts) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= N) return;
-  double c = 0.0;
-  for (int t = 0; t < T; ++t)
-    for (int r = 0; r < k; ++r)
-      if (ids[t * k + r] == e) c += w.n_rank_weights ? w.rank_weights[r] : 1.0;
-  counts[e] = c;
 }
 
 cudaError_t launch_topk(const double* vals, int T, int N, int k, int32_t* ids, double* out, cudaStream_t s) {

@@ -35,7 +35,7 @@ def test_library_exports_every_header_symbol():
 def test_status_strings_and_version():
     from paper_2411_08982_b200 import _native
     lib = _native.load()
-    assert lib.lynx_abi_version() == 1
+    assert lib.lynx_abi_version() == _native.ABI_VERSION
     assert lib.lynx_status_string(0) == b"ok"
     assert lib.lynx_status_string(-3) == b"min_experts must be >= top_k"
 

@@ -56,7 +56,8 @@ def test_permute_order_matches_reference_dispatch():
     nat.lib().lynx_dispatch_caps(T, N, k, ctypes.byref(max_seg), ctypes.byref(rows_cap))
     S, R = max_seg.value, rows_cap.value
     buf = {n: torch.full(s, -7, dtype=dt, device="cuda") for n, s, dt in [
-        ("n_seg", (1,), torch.int32), ("n_used", (1,), torch.int32), ("seg_expert", (S,), torch.int32),
+        ("n_seg", (1,), torch.int32), ("n_used", (1,), torch.int32), ("n_rows", (1,), torch.int32),
+        ("seg_expert", (S,), torch.int32),
         ("seg_row", (S,), torch.int32), ("seg_count", (S,), torch.int32), ("perm_token", (R,), torch.int32),
         ("perm_weight", (R,), torch.float32), ("tok_rows", (T, k), torch.int32),
         ("tok_weight", (T, k), torch.float32)]}
