@@ -151,13 +151,14 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.perm_weight = take(sizeof(float) * c.rows_cap);
   p.tok_rows = take(sizeof(int32_t) * T * k);
   p.tok_weight = take(sizeof(float) * T * k);
-  // ticket + phase-0 done per segment + split chain per (segment, m-tile) +
-  // segments done per (m-tile, warp quarter)
-  p.n_counters = 1 + c.max_seg + c.max_seg * g.tiles2 + g.tiles2 * 4;
+  // ticket + phase-0 done per segment + splits landed per (segment, m-tile,
+  // warp quarter) + segments done per (m-tile, warp quarter)
+  p.n_counters = 1 + c.max_seg + c.max_seg * g.tiles2 * 4 + g.tiles2 * 4;
   p.counters = take(sizeof(int32_t) * p.n_counters);
   p.x_perm = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * d);
   p.h = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * ff);
-  p.y = take(sizeof(float) * static_cast<size_t>(c.rows_cap) * d);
+  // split-K partial slots [split2][rows_cap][d]; slot 0 ends up holding Y
+  p.y = take(sizeof(float) * static_cast<size_t>(g.split2) * c.rows_cap * d);
   p.total = off + 256;  // slack for base alignment
   return p;
 }

@@ -12,12 +12,14 @@
 //        epilogue h = silu(gate) * up -> H[seg rows, 64 features] (bf16).
 //        TANH2:  epilogue h = tanh(acc) -> H[seg rows, 128 features].
 //   phase-1 unit (seg, mt, s):    D[128 x n] = W2[e][mt*128 : +128, K_s] . H_seg[:, K_s]^T
-//        epilogue: Y[seg rows][mt*128 : +128] (f32) = D for s = 0, else
-//        Y += D after split s-1 has published -- a fixed summation order,
-//        so results are bit-reproducible without float atomics.  When the
-//        last split of the last segment of an m-tile lands, that warp
-//        applies the combine (simulator.py:101-112) for its 32 columns:
-//        out[t] = hidden[t] + sum_j w_tj * Y[row_tj], experts ascending.
+//        epilogue: slot[s][seg rows][mt*128 : +128] = D (f32), no waiting.
+//        The last split to land for (segment, m-tile, warp quarter) sums the
+//        slots in the fixed order 0..S-1 into slot 0 -- bit-reproducible
+//        without float atomics -- and the last segment to finish a column
+//        slice applies the combine (simulator.py:101-112) for its 32
+//        columns: out[t] = hidden[t] + sum_j w_tj * Y[row_tj], experts
+//        ascending.  Nothing on the streaming path ever blocks on another CTA
+//        except phase-1 loads of H (which queue order makes ready).
 //
 // Swap-AB: weight rows are the MMA M (=128) dimension, the segment's tokens
 // the MMA N dimension (16..256, rounded to 16), so decode streams each used
@@ -79,33 +81,60 @@ __device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u,
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.f + __expf(-g)) * u; }
 
+// slot0[row][r] = ((slot0 + slot1) + slot2) + ... for the segment's rows:
+// split-K partials summed in a fixed order (bit-reproducible).
+__device__ __noinline__ void reduce_splits(const FfnParams& p, int row0, int n, int r) {
+  const size_t stride = static_cast<size_t>(p.rows_cap) * p.d;
+  float* base = p.partial + static_cast<size_t>(row0) * p.d + r;
+  for (int t0 = 0; t0 < n; t0 += 8) {
+    float acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = t0 + u < n ? __ldcg(base + static_cast<size_t>(t0 + u) * p.d) : 0.f;
+    for (int s0 = 1; s0 < p.split2; s0 += 8) {
+      float v[8][8];  // 64 independent loads in flight
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[s][u] = (s0 + s < p.split2 && t0 + u < n)
+                        ? __ldcg(base + (s0 + s) * stride + static_cast<size_t>(t0 + u) * p.d)
+                        : 0.f;
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + s < p.split2) acc[u] += v[s][u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < n) __stcg(base + static_cast<size_t>(t0 + u) * p.d, acc[u]);
+  }
+}
+
 // Combine for one output column r (all tokens): residual + experts in
 // ascending order, the reference's accumulation order (simulator.py:101-112).
 __device__ __noinline__ void combine_column(const FfnParams& p, int r) {
   const float* Y = p.partial + r;
-  for (int t0 = 0; t0 < p.T; t0 += 4) {
-    float acc[4];
+  const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(p.hidden);
+  for (int t0 = 0; t0 < p.T; t0 += 8) {
+    float acc[8], y[8][LYNX_MAX_TOPK], w[8][LYNX_MAX_TOPK];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const int t = t0 + u;
-      acc[u] = 0.f;
-      if (t < p.T && p.hidden)
-        acc[u] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.hidden)[static_cast<size_t>(t) * p.d + r]);
-    }
-    for (int j = 0; j < p.k; ++j) {
-      float y[4], w[4];
+      acc[u] = (t < p.T && X) ? __bfloat162float(X[static_cast<size_t>(t) * p.d + r]) : 0.f;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int t = t0 + u;
-        const int row = t < p.T ? p.tok_rows[t * p.k + j] : -1;
-        w[u] = row >= 0 ? p.tok_weight[t * p.k + j] : 0.f;
-        y[u] = row >= 0 ? __ldcg(Y + static_cast<size_t>(row) * p.d) : 0.f;
+      for (int j = 0; j < LYNX_MAX_TOPK; ++j) {
+        const int row = (t < p.T && j < p.k) ? p.tok_rows[t * p.k + j] : -1;
+        w[u][j] = row >= 0 ? p.tok_weight[t * p.k + j] : 0.f;
+        y[u][j] = row >= 0 ? __ldcg(Y + static_cast<size_t>(row) * p.d) : 0.f;
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += w[u] * y[u];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int j = 0; j < LYNX_MAX_TOPK; ++j) acc[u] += w[u][j] * y[u][j];  // rows are -1-padded at the end
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
       const int t = t0 + u;
       if (t >= p.T) break;
       const size_t o = static_cast<size_t>(t) * p.d + r;
@@ -311,45 +340,46 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           }
         }
       } else {
-        // ---- phase 1: chained split-K accumulation into Y, then combine
+        // ---- phase 1: split-K partial -> slot s; the last split of this
+        //      (segment, m-tile, warp quarter) to land sums slots 0..S-1 in
+        //      order into slot 0; the last segment then applies the combine.
         const int r = U.mt * 128 + q * 32 + lane;  // output column (d index)
         const bool rv = r < p.d;
-        float* Y = p.partial + static_cast<size_t>(U.row0) * p.d + r;
-        int* chain = p.counters + 1 + p.max_seg + U.seg * p.tiles2 + U.mt;
-        if (U.split > 0) {
-          Watchdog wd;
-          while (ld_acquire_gpu(chain) < 4 * U.split) wd.tick(9);
-        }
+        const size_t slot_stride = static_cast<size_t>(p.rows_cap) * p.d;
+        float* mine = p.partial + U.split * slot_stride + static_cast<size_t>(U.row0) * p.d + r;
         for (int c0 = 0; c0 < U.nmma; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(tb + c0, v);
           tmem_ld_wait();
-          float prev[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            prev[j] = (U.split > 0 && c0 + j < U.n && rv) ? __ldcg(Y + static_cast<size_t>(c0 + j) * p.d) : 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < U.n && rv) __stcg(Y + static_cast<size_t>(c0 + j) * p.d, prev[j] + __uint_as_float(v[j]));
+            if (c0 + j < U.n && rv) __stcg(mine + static_cast<size_t>(c0 + j) * p.d, __uint_as_float(v[j]));
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) red_release_gpu_add(chain, 1);
-        if (U.split == p.split2 - 1) {
-          int* done = p.counters + 1 + p.max_seg + p.max_seg * p.tiles2 + U.mt * 4 + q;
-          int last = 0;
-          if (lane == 0) last = atom_add_acq_rel_gpu(done, 1) == nseg - 1;
-          last = __shfl_sync(0xffffffffu, last, 0);
-          if (last && rv) {
-            fence_acq_rel_gpu();
-            combine_column(p, r);
-          }
-        }
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
+        __threadfence();
+        __syncwarp();
+        int last = 1;
+        if (p.split2 > 1) {
+          int* cnt = p.counters + 1 + p.max_seg + (U.seg * p.tiles2 + U.mt) * 4 + q;
+          if (lane == 0) last = atom_add_acq_rel_gpu(cnt, 1) == p.split2 - 1;
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (!last) continue;
+          fence_acq_rel_gpu();
+          if (rv) reduce_splits(p, U.row0, U.n, r);
+          __threadfence();
+          __syncwarp();
+        }
+        int* done = p.counters + 1 + p.max_seg + p.max_seg * p.tiles2 * 4 + U.mt * 4 + q;
+        if (lane == 0) last = atom_add_acq_rel_gpu(done, 1) == nseg - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last && rv) {
+          fence_acq_rel_gpu();
+          combine_column(p, r);
+        }
         continue;
       }
       tc_fence_before();

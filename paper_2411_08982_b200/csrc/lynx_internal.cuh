@@ -13,7 +13,7 @@
 
 namespace lynx {
 
-constexpr int kSelectThreads = 512;
+constexpr int kSelectThreads = 1024;  // one warp per token, 32 tokens at a time
 constexpr size_t kSelectMaxSmem = 200 * 1024;
 
 // ------------------------------------------------- programmatic dependent launch

@@ -17,9 +17,11 @@
 //   accuracy_policy            policy.py:287-338
 //   dispatch order             simulator.py:104-112
 //
-// Latency, not bandwidth, bounds these kernels (a decode batch is a few KB
-// of routing state), so K1 is one CTA that stages every per-token array in
-// shared memory and never chains dependent global loads.
+// These kernels are latency-bound (a decode batch is a few KB of routing
+// state): K1 is one CTA, one warp per token with lanes over experts, every
+// per-token array staged in shared memory, and compact (non-inlined) code --
+// the kernel runs once per layer from a cold instruction cache, so code
+// size is latency.
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -27,10 +29,12 @@
 
 namespace lynx {
 
+constexpr unsigned kFull = 0xffffffffu;
+
 // numpy's pairwise float64 summation (oracle.pairwise_sum): < 8 terms added
 // left to right; <= 128 terms with 8 strided partials folded pairwise plus
 // the tail; longer runs split at an 8-aligned midpoint.
-__device__ double np_pairwise_sum(const double* a, int n) {
+__device__ __noinline__ double np_pairwise_sum(const double* a, int n) {
   if (n < 8) {
     double acc = 0.0;
     for (int i = 0; i < n; ++i) acc += a[i];
@@ -38,13 +42,10 @@ __device__ double np_pairwise_sum(const double* a, int n) {
   }
   if (n <= 128) {
     double r[8];
-#pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = a[j];
     const int body = n - (n % 8);
-    for (int i = 8; i < body; i += 8) {
-#pragma unroll
+    for (int i = 8; i < body; i += 8)
       for (int j = 0; j < 8; ++j) r[j] += a[i + j];
-    }
     double acc = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
     for (int i = body; i < n; ++i) acc += a[i];
     return acc;
@@ -54,27 +55,124 @@ __device__ double np_pairwise_sum(const double* a, int n) {
   return np_pairwise_sum(a, half) + np_pairwise_sum(a + half, n - half);
 }
 
+// Same sum computed by a warp: lanes 0..7 each run one strided partial in
+// numpy's order; lane 0 folds.  Result broadcast to all lanes.
+__device__ __noinline__ double warp_pairwise_sum(const double* a, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n < 8 || n > 128) {
+    double acc = lane == 0 ? np_pairwise_sum(a, n) : 0.0;
+    return __shfl_sync(kFull, acc, 0);
+  }
+  const int body = n - (n % 8);
+  double r = 0.0;
+  if (lane < 8) {
+    r = a[lane];
+    for (int i = 8 + lane; i < body; i += 8) r += a[i];
+  }
+  double part[8];
+  for (int j = 0; j < 8; ++j) part[j] = __shfl_sync(kFull, r, j);
+  double acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+  for (int i = body; i < n; ++i) acc += a[i];
+  return acc;  // identical on every lane
+}
+
 __device__ __forceinline__ uint64_t expert_mask_all(int N) { return N == 64 ? ~0ull : ((1ull << N) - 1); }
 
-// Best expert in `cand` by (probability desc, index asc); -1 if none.
-__device__ __forceinline__ int best_of(const double* p, uint64_t cand, int N) {
-  int best = -1;
-  double bp = 0.0;
-  for (int e = 0; e < N; ++e) {
-    if ((cand >> e) & 1ull) {
-      const double v = p[e];
-      if (best < 0 || v > bp) {
-        best = e;
-        bp = v;
+// Warp argmax over the experts in `cand` by (value desc, index asc); each
+// lane holds experts lane and lane+32.  Returns the index (-1 if none) and
+// writes the value to *bv.  All lanes get the result.
+__device__ __noinline__ int warp_best(double v0, double v1, uint64_t cand, double* bv) {
+  const int lane = threadIdx.x & 31;
+  double best = -1.0;
+  int bi = -1;
+  if ((cand >> lane) & 1ull) {
+    best = v0;
+    bi = lane;
+  }
+  if (((cand >> (lane + 32)) & 1ull) && (bi < 0 || v1 > best)) {
+    best = v1;
+    bi = lane + 32;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(kFull, best, off);
+    const int oi = __shfl_xor_sync(kFull, bi, off);
+    if (oi >= 0 && (bi < 0 || ov > best || (ov == best && oi < bi))) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  *bv = best;
+  return bi;
+}
+
+__device__ __forceinline__ double lane_value(double v0, double v1, int e) {
+  const double a = __shfl_sync(kFull, v0, e & 31);
+  const double b = __shfl_sync(kFull, v1, e & 31);
+  return e < 32 ? a : b;
+}
+
+// Softmax + stable top-k + confidence for one token (router.py:141-187,
+// 125-138).  With z == null the row p and ids/probs are inputs.
+__device__ __noinline__ void route_token(const double* z, double* p, int N, int k, int metric, int32_t* ids,
+                                         double* probs, double* conf, int* flags) {
+  const int lane = threadIdx.x & 31;
+  const int e0 = lane, e1 = lane + 32;
+  const uint64_t all = expert_mask_all(N);
+  double v0 = 0.0, v1 = 0.0;
+  if (z) {
+    const double z0 = e0 < N ? z[e0] : 0.0, z1 = e1 < N ? z[e1] : 0.0;
+    const bool bad = (e0 < N && !isfinite(z0)) || (e1 < N && !isfinite(z1));
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(flags, LYNX_FLAG_NONFINITE);
+    double m = e0 < N ? z0 : -INFINITY;
+    if (e1 < N && z1 > m) m = z1;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(kFull, m, off);
+      m = o > m ? o : m;
+    }
+    if (e0 < N) p[e0] = exp(z0 - m);
+    if (e1 < N) p[e1] = exp(z1 - m);
+    __syncwarp();
+    const double s = warp_pairwise_sum(p, N);
+    if (e0 < N) p[e0] = p[e0] / s;
+    if (e1 < N) p[e1] = p[e1] / s;
+    __syncwarp();
+  }
+  v0 = e0 < N ? p[e0] : 0.0;
+  v1 = e1 < N ? p[e1] : 0.0;
+  if (z) {
+    uint64_t taken = 0;
+    for (int r = 0; r < k; ++r) {
+      double bv;
+      const int b = warp_best(v0, v1, all & ~taken, &bv);
+      taken |= 1ull << b;
+      if (lane == 0) {
+        ids[r] = b;
+        probs[r] = bv;
       }
     }
   }
-  return best;
+  double top1;
+  const int first = warp_best(v0, v1, all, &top1);
+  double c = top1;
+  if (metric == LYNX_CONF_MARGIN) {
+    if (N == 1) {
+      c = v0;  // lane 0 holds p[0]
+      c = __shfl_sync(kFull, c, 0);
+    } else {  // np.sort(full)[-1] - np.sort(full)[-2]
+      double second;
+      warp_best(v0, v1, all & ~(1ull << first), &second);
+      c = top1 - second;
+    }
+  }
+  if (lane == 0) *conf = c;
 }
 
-// remap_tokens for one token (policy.py:171-210).
-__device__ __forceinline__ void remap_one(const int32_t* ids, const double* p, int k, int N, uint64_t keep,
-                                          int32_t* assigned, double* weights, int* flags) {
+// remap_tokens for one token (policy.py:171-210), one warp.
+__device__ __noinline__ void remap_token(const int32_t* ids, const double* p, int k, int N, uint64_t keep,
+                                         int32_t* assigned, double* weights, int* flags) {
+  const int lane = threadIdx.x & 31;
+  const double v0 = lane < N ? p[lane] : 0.0;
+  const double v1 = lane + 32 < N ? p[lane + 32] : 0.0;
   uint64_t occupied = 0;
   for (int r = 0; r < k; ++r) {
     const int e = ids[r];
@@ -84,28 +182,31 @@ __device__ __forceinline__ void remap_one(const int32_t* ids, const double* p, i
   for (int r = 0; r < k; ++r) {
     int e = ids[r];
     if (!((keep >> e) & 1ull)) {
-      int pick = best_of(p, keep & ~occupied, N);
-      if (pick < 0) pick = best_of(p, keep, N);  // collapse (policy.py:197-200)
+      double bv;
+      int pick = warp_best(v0, v1, keep & ~occupied, &bv);
+      if (pick < 0) pick = warp_best(v0, v1, keep, &bv);  // collapse (policy.py:197-200)
       e = pick;
       occupied |= 1ull << e;
     }
-    assigned[r] = e;
-    slot_p[r] = p[e];
+    slot_p[r] = lane_value(v0, v1, e);
+    if (lane == 0) assigned[r] = e;
   }
-  const double total = np_pairwise_sum(slot_p, k);
-  if (!(total > 0.0)) atomicOr(flags, LYNX_FLAG_ZERO_MASS);
-  for (int r = 0; r < k; ++r) weights[r] = slot_p[r] / total;
+  if (lane == 0) {
+    const double total = np_pairwise_sum(slot_p, k);
+    if (!(total > 0.0)) atomicOr(flags, LYNX_FLAG_ZERO_MASS);
+    for (int r = 0; r < k; ++r) weights[r] = slot_p[r] / total;
+  }
 }
 
 // ------------------------------------------------------------- dispatch plan
 // forward_layer's grouping (simulator.py:104-112): used experts ascending,
 // each expert's token rows ascending, a token's duplicate slots on one expert
 // merged (weights summed in slot order).  Rows of expert e occupy
-// [base[e], base[e] + cnt[e]) in the permuted buffer, base 16-aligned;
-// segments split an expert at LYNX_SEG_ROWS rows.  Called by every thread of
-// one CTA; `asg`/`w` may live in shared or global memory.
-__device__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N, int k, const PlanOut& o,
-                              uint32_t* s_bits, int* s_prefix) {
+// [base[e], base[e] + cnt[e]) of the permuted buffer, base 16-aligned;
+// segments split an expert at LYNX_SEG_ROWS rows.  Called by every thread
+// of one CTA; `asg`/`w` may live in shared or global memory.
+__device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N, int k,
+                                           const PlanOut& o, uint32_t* s_bits, int* s_prefix) {
   __shared__ int s_cnt[LYNX_MAX_EXPERTS];
   __shared__ int s_base[LYNX_MAX_EXPERTS];
   const int W = (T + 31) >> 5;
@@ -193,7 +294,7 @@ __device__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N,
   }
 }
 
-// Shared-memory carve-up of K1 (host computes the same with select_smem_bytes).
+// Shared-memory carve-up of K1 (the host computes the same size).
 struct SelectSmem {
   size_t p, conf, ids, probs, asg, w, imp, bits, prefix, total;
 };
@@ -224,6 +325,109 @@ __host__ __device__ inline SelectSmem select_smem(int T, int N, int k, bool stag
   return s;
 }
 
+// Batch-level policy: vote, retention order, retained set (policy.py:116-148,
+// 232-338).  Writes s_keep / s_counts; returns via s_clipped.
+__device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* IDS, const double* CONF, uint8_t* IMP,
+                                          int* s_keep, double* s_counts, int* s_icount, int* s_rank, int* s_order,
+                                          int* s_nq, int* s_clipped) {
+  const int T = a.T, N = a.N, k = a.k, tid = threadIdx.x, nthr = blockDim.x;
+  const bool accuracy = a.pol.mode == LYNX_POLICY_ACCURACY;
+  if (accuracy) {  // select_important_tokens
+    const double tau = a.pol.confidence_threshold;
+    int local = 0;
+    for (int t = tid; t < T; t += nthr) {
+      const bool q = CONF[t] >= tau;
+      IMP[t] = q ? 1 : 0;
+      local += q;
+    }
+    if (local) atomicAdd(s_nq, local);
+    __syncthreads();
+    const int nq = *s_nq;
+    const int S = a.pol.sample_threshold;
+    if (nq == 0) {
+      if (tid == 0) {
+        int best = 0;
+        for (int t = 1; t < T; ++t)
+          if (CONF[t] > CONF[best]) best = t;
+        IMP[best] = 1;
+      }
+    } else if (nq > S) {
+      // keep the S most confident (conf desc, t asc); ranks read CONF only,
+      // so marking drops in bit 1 is race-free
+      for (int t = tid; t < T; t += nthr) {
+        if (!IMP[t]) continue;
+        const double ct = CONF[t];
+        int rank = 0;
+        for (int u = 0; u < T; ++u) {
+          const double cu = CONF[u];
+          rank += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
+        }
+        if (rank >= S) IMP[t] |= 2;
+      }
+      __syncthreads();
+      for (int t = tid; t < T; t += nthr) IMP[t] = IMP[t] == 1;
+    }
+    __syncthreads();
+  }
+  // Unit votes are integers: order-free atomics are exact.  Rank-weighted
+  // votes are float sums and keep numpy's slot order (thread per expert).
+  if (!a.pol.n_rank_weights) {
+    for (int i = tid; i < T * k; i += nthr)
+      if (!accuracy || IMP[i / k]) atomicAdd(&s_icount[IDS[i]], 1);
+    __syncthreads();
+    for (int e = tid; e < N; e += nthr) s_counts[e] = static_cast<double>(s_icount[e]);
+  } else {
+    for (int e = tid; e < N; e += nthr) {
+      double c = 0.0;
+      for (int t = 0; t < T; ++t) {
+        if (accuracy && !IMP[t]) continue;
+        for (int r = 0; r < k; ++r)
+          if (IDS[t * k + r] == e) c += a.pol.rank_weights[r];
+      }
+      s_counts[e] = c;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < N; e += nthr) {  // retention order: count desc, index asc
+    const double ce = s_counts[e];
+    int rank = 0;
+    for (int f = 0; f < N; ++f) {
+      const double cf = s_counts[f];
+      rank += (cf > ce || (cf == ce && f < e)) ? 1 : 0;
+    }
+    s_rank[e] = rank;
+    s_order[rank] = e;
+  }
+  __syncthreads();
+  if (!accuracy) {  // latency_policy
+    const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
+    const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
+    for (int e = tid; e < N; e += nthr) s_keep[e] = s_rank[e] < N - eff;
+    if (tid == 0) *s_clipped = eff != a.pol.drop_count;
+  } else {  // accuracy_policy
+    const int budget = a.pol.freq_keep_budget < N ? a.pol.freq_keep_budget : N;
+    for (int e = tid; e < N; e += nthr) s_keep[e] = (s_counts[e] > 0.0 && s_rank[e] < budget) ? 1 : 0;
+    __syncthreads();
+    for (int t = tid; t < T; t += nthr)
+      if (IMP[t]) s_keep[IDS[t * k]] = 1;
+    __syncthreads();
+    if (tid == 0) {
+      int cnt = 0;
+      for (int e = 0; e < N; ++e) cnt += s_keep[e];
+      int padded = 0;
+      for (int pos = 0; pos < N && cnt < a.floor_keep; ++pos) {
+        const int e = s_order[pos];
+        if (!s_keep[e]) {
+          s_keep[e] = 1;
+          ++cnt;
+          padded = 1;
+        }
+      }
+      *s_clipped = padded;
+    }
+  }
+}
+
 // ------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs a) {
   __shared__ double s_counts[LYNX_MAX_EXPERTS];
@@ -236,10 +440,9 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   extern __shared__ __align__(16) uint8_t s_dyn[];
 
   griddep_launch_dependents();
-  griddep_wait();  // logits come from K0 (programmatic dependent launch)
-
   const int T = a.T, N = a.N, k = a.k;
   const int tid = threadIdx.x, nthr = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
   const SelectSmem L = select_smem(T, N, k, a.stage, a.plan.enabled);
   // Working arrays: shared memory when they fit, else the caller's outputs.
   double* P = a.stage ? reinterpret_cast<double*>(s_dyn + L.p) : a.full;
@@ -256,6 +459,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
     s_clipped = 0;
   }
   for (int e = tid; e < N; e += nthr) s_icount[e] = 0;
+  griddep_wait();  // logits come from K0 (programmatic dependent launch)
   if (!a.logits && a.stage) {  // apply_policy on a given selection: stage it
     for (int i = tid; i < T * N; i += nthr) P[i] = a.full[i];
     for (int i = tid; i < T * k; i += nthr) {
@@ -265,58 +469,15 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   }
   __syncthreads();
 
-  // 1) softmax + top-k (when routing from logits) + confidence, thread per token.
-  for (int t = tid; t < T; t += nthr) {
-    double* p = P + static_cast<size_t>(t) * N;
-    if (a.logits) {
-      const double* z = a.logits + static_cast<size_t>(t) * N;
-#pragma unroll 8
-      for (int i = 0; i < N; ++i) p[i] = z[i];  // independent loads, staged
-      double m = p[0];
-      bool finite = true;
-      for (int i = 0; i < N; ++i) {
-        const double v = p[i];
-        finite &= isfinite(v);
-        m = v > m ? v : m;
-      }
-      if (!finite) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
-      for (int i = 0; i < N; ++i) p[i] = exp(p[i] - m);
-      const double s = np_pairwise_sum(p, N);
-      for (int i = 0; i < N; ++i) p[i] = p[i] / s;
-      uint64_t taken = 0;
-      for (int r = 0; r < k; ++r) {
-        const int b = best_of(p, expert_mask_all(N) & ~taken, N);
-        taken |= 1ull << b;
-        IDS[t * k + r] = b;
-        PROBS[t * k + r] = p[b];
-      }
-    }
-    double top1 = p[0];
-    int first = 0;
-    for (int i = 1; i < N; ++i)
-      if (p[i] > top1) {
-        top1 = p[i];
-        first = i;
-      }
-    double c = top1;
-    if (a.pol.confidence_metric == LYNX_CONF_MARGIN) {
-      if (N == 1) {
-        c = p[0];
-      } else {  // np.sort(full)[-1] - np.sort(full)[-2]
-        double second = -1.0;
-        for (int i = 0; i < N; ++i)
-          if (i != first && p[i] > second) second = p[i];
-        c = top1 - second;
-      }
-    }
-    CONF[t] = c;
-  }
+  // 1) softmax + top-k + confidence: one warp per token
+  for (int t = warp; t < T; t += nwarps)
+    route_token(a.logits ? a.logits + static_cast<size_t>(t) * N : nullptr, P + static_cast<size_t>(t) * N, N, k,
+                a.pol.confidence_metric, IDS + t * k, PROBS + t * k, CONF + t, &s_flags);
   __syncthreads();
 
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
   const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
-  if (!run_policy) {
-    // full_retain_mask: identity, weights = probs / row sum.
+  if (!run_policy) {  // full_retain_mask: identity, weights = probs / row sum
     for (int t = tid; t < T; t += nthr) {
       const double s = np_pairwise_sum(PROBS + t * k, k);
       for (int r = 0; r < k; ++r) {
@@ -330,104 +491,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
       s_counts[e] = 0.0;
     }
   } else {
-    // 2a) important tokens (accuracy) -- select_important_tokens.
-    if (accuracy) {
-      const double tau = a.pol.confidence_threshold;
-      int local = 0;
-      for (int t = tid; t < T; t += nthr) {
-        const bool q = CONF[t] >= tau;
-        IMP[t] = q ? 1 : 0;
-        local += q;
-      }
-      if (local) atomicAdd(&s_nq, local);
-      __syncthreads();
-      const int nq = s_nq;
-      const int S = a.pol.sample_threshold;
-      if (nq == 0) {
-        if (tid == 0) {
-          int best = 0;
-          for (int t = 1; t < T; ++t)
-            if (CONF[t] > CONF[best]) best = t;
-          IMP[best] = 1;
-        }
-      } else if (nq > S) {
-        // keep the S most confident qualifying tokens (conf desc, t asc);
-        // ranks come from CONF alone, so marking drops in bit 1 is race-free.
-        for (int t = tid; t < T; t += nthr) {
-          if (!IMP[t]) continue;
-          const double ct = CONF[t];
-          int rank = 0;
-          for (int u = 0; u < T; ++u) {
-            const double cu = CONF[u];
-            rank += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
-          }
-          if (rank >= S) IMP[t] |= 2;
-        }
-        __syncthreads();
-        for (int t = tid; t < T; t += nthr) IMP[t] = IMP[t] == 1;
-      }
-      __syncthreads();
-    }
-    // 2b) vote tally over all (or the important) tokens.  Unit votes are
-    //     integers: order-free atomics are exact.  Rank-weighted votes are
-    //     float sums and keep numpy's slot order (one thread per expert).
-    if (!a.pol.n_rank_weights) {
-      for (int i = tid; i < T * k; i += nthr)
-        if (!accuracy || IMP[i / k]) atomicAdd(&s_icount[IDS[i]], 1);
-      __syncthreads();
-      for (int e = tid; e < N; e += nthr) s_counts[e] = static_cast<double>(s_icount[e]);
-    } else {
-      for (int e = tid; e < N; e += nthr) {
-        double c = 0.0;
-        for (int t = 0; t < T; ++t) {
-          if (accuracy && !IMP[t]) continue;
-          for (int r = 0; r < k; ++r)
-            if (IDS[t * k + r] == e) c += a.pol.rank_weights[r];
-        }
-        s_counts[e] = c;
-      }
-    }
-    __syncthreads();
-    // 2c) retention order: count desc, index asc.
-    for (int e = tid; e < N; e += nthr) {
-      const double ce = s_counts[e];
-      int rank = 0;
-      for (int f = 0; f < N; ++f) {
-        const double cf = s_counts[f];
-        rank += (cf > ce || (cf == ce && f < e)) ? 1 : 0;
-      }
-      s_rank[e] = rank;
-      s_order[rank] = e;
-    }
-    __syncthreads();
-    if (!accuracy) {
-      // latency_policy: drop the `eff` least-voted experts.
-      const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
-      const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
-      for (int e = tid; e < N; e += nthr) s_keep[e] = s_rank[e] < N - eff;
-      if (tid == 0) s_clipped = eff != a.pol.drop_count;
-    } else {
-      const int budget = a.pol.freq_keep_budget < N ? a.pol.freq_keep_budget : N;
-      for (int e = tid; e < N; e += nthr) s_keep[e] = (s_counts[e] > 0.0 && s_rank[e] < budget) ? 1 : 0;
-      __syncthreads();
-      for (int t = tid; t < T; t += nthr)
-        if (IMP[t]) s_keep[IDS[t * k]] = 1;
-      __syncthreads();
-      if (tid == 0) {
-        int cnt = 0;
-        for (int e = 0; e < N; ++e) cnt += s_keep[e];
-        int padded = 0;
-        for (int pos = 0; pos < N && cnt < a.floor_keep; ++pos) {
-          const int e = s_order[pos];
-          if (!s_keep[e]) {
-            s_keep[e] = 1;
-            ++cnt;
-            padded = 1;
-          }
-        }
-        s_clipped = padded;
-      }
-    }
+    batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
   }
   __syncthreads();
   if (tid == 0) {
@@ -438,15 +502,15 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   }
   __syncthreads();
 
-  // 3) remap every token onto the retained set.
+  // 2) remap every token onto the retained set: one warp per token
   if (run_policy) {
     const uint64_t keep = s_keepmask;
-    for (int t = tid; t < T; t += nthr)
-      remap_one(IDS + t * k, P + static_cast<size_t>(t) * N, k, N, keep, ASG + t * k, WT + t * k, &s_flags);
+    for (int t = warp; t < T; t += nwarps)
+      remap_token(IDS + t * k, P + static_cast<size_t>(t) * N, k, N, keep, ASG + t * k, WT + t * k, &s_flags);
   }
   __syncthreads();
 
-  // 4) outputs
+  // 3) outputs
   if (a.stage) {
     if (a.logits) {
       for (int i = tid; i < T * N; i += nthr) a.full[i] = P[i];
@@ -469,7 +533,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
     for (int t = tid; t < T; t += nthr) a.important[t] = accuracy ? IMP[t] : 0;
   if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
 
-  // 5) dispatch plan for K2/K3 (layer path)
+  // 4) dispatch plan for K2/K3 (layer path)
   if (a.plan.enabled)
     plan_dispatch(ASG, WT, T, N, k, a.plan, reinterpret_cast<uint32_t*>(s_dyn + L.bits),
                   reinterpret_cast<int*>(s_dyn + L.prefix));
@@ -486,7 +550,7 @@ __global__ void __launch_bounds__(kSelectThreads) plan_kernel(const int32_t* asg
                 reinterpret_cast<int*>(s_dyn + sizeof(uint32_t) * N * W));
 }
 
-// remap_tokens on a caller-supplied retained mask.
+// remap_tokens on a caller-supplied retained mask; one warp per token.
 __global__ void remap_kernel(const int32_t* ids, const double* full, int T, int N, int k, const uint8_t* retained,
                              int32_t* assigned, double* weights, int32_t* flags) {
   __shared__ unsigned long long s_keep;
@@ -499,24 +563,30 @@ __global__ void remap_kernel(const int32_t* ids, const double* full, int T, int 
     s_flags = 0;
   }
   __syncthreads();
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
-    remap_one(ids + t * k, full + static_cast<size_t>(t) * N, k, N, s_keep, assigned + t * k, weights + t * k,
-              &s_flags);
+  const int warps = blockDim.x >> 5;
+  for (int t = blockIdx.x * warps + (threadIdx.x >> 5); t < T; t += gridDim.x * warps)
+    remap_token(ids + t * k, full + static_cast<size_t>(t) * N, k, N, s_keep, assigned + t * k, weights + t * k,
+                &s_flags);
   __syncthreads();
   if (threadIdx.x == 0 && s_flags) atomicOr(flags, s_flags);
 }
 
 // top_k_select (router.py:157-171) over float64 rows: (value desc, index asc).
 __global__ void topk_kernel(const double* vals, int T, int N, int k, int32_t* ids, double* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const double* p = vals + static_cast<size_t>(t) * N;
-  uint64_t taken = 0;
-  for (int r = 0; r < k; ++r) {
-    const int b = best_of(p, expert_mask_all(N) & ~taken, N);
-    taken |= 1ull << b;
-    ids[t * k + r] = b;
-    out[t * k + r] = p[b];
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int t = blockIdx.x * warps + (threadIdx.x >> 5); t < T; t += gridDim.x * warps) {
+    const double* p = vals + static_cast<size_t>(t) * N;
+    const double v0 = lane < N ? p[lane] : 0.0, v1 = lane + 32 < N ? p[lane + 32] : 0.0;
+    uint64_t taken = 0;
+    for (int r = 0; r < k; ++r) {
+      double bv;
+      const int b = warp_best(v0, v1, expert_mask_all(N) & ~taken, &bv);
+      taken |= 1ull << b;
+      if (lane == 0) {
+        ids[t * k + r] = b;
+        out[t * k + r] = bv;
+      }
+    }
   }
 }
 
@@ -581,7 +651,7 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __re
   for (int n = 0; n < 9; ++n) {
     float v = n < 8 ? acc[n] : ss;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     if (lane == 0) s_red[warp][n] = v;
   }
   __syncthreads();
@@ -611,17 +681,23 @@ bool select_can_stage(int T, int N, int k, bool plan) {
   return select_smem(T, N, k, true, plan).total <= kSelectMaxSmem;
 }
 
+static cudaError_t allow_big_smem(const void* fn, int& configured_device) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_device == dev) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kSelectMaxSmem));
+  if (e == cudaSuccess) configured_device = dev;
+  return e;
+}
+
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
   const size_t smem = select_smem_bytes(a.T, a.N, a.k, a.stage, a.plan.enabled);
   if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
-  static int configured_device = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured_device != dev) {
-    cudaError_t e = cudaFuncSetAttribute(route_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSelectMaxSmem));
+  static int configured = -1;
+  if (smem > 48 * 1024) {
+    cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_kernel), configured);
     if (e != cudaSuccess) return e;
-    configured_device = dev;
   }
   return launch_pdl(route_select_kernel, dim3(1), dim3(kSelectThreads), smem, s, a);
 }
@@ -630,27 +706,23 @@ cudaError_t launch_plan(const int32_t* asg, const double* w, int T, int N, int k
   const int W = (T + 31) / 32;
   const size_t smem = static_cast<size_t>(N) * W * 8;
   if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
-  static int configured_device = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured_device != dev) {
-    cudaError_t e = cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSelectMaxSmem));
+  static int configured = -1;
+  if (smem > 48 * 1024) {
+    cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(plan_kernel), configured);
     if (e != cudaSuccess) return e;
-    configured_device = dev;
   }
   return launch_pdl(plan_kernel, dim3(1), dim3(kSelectThreads), smem, s, asg, w, T, N, k, o);
 }
 
 cudaError_t launch_remap(const int32_t* ids, const double* full, int T, int N, int k, const uint8_t* retained,
                          int32_t* assigned, double* weights, int32_t* flags, cudaStream_t s) {
-  const int blocks = (T + 255) / 256;
+  const int blocks = (T + 7) / 8;
   remap_kernel<<<blocks, 256, 0, s>>>(ids, full, T, N, k, retained, assigned, weights, flags);
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk(const double* vals, int T, int N, int k, int32_t* ids, double* out, cudaStream_t s) {
-  topk_kernel<<<(T + 127) / 128, 128, 0, s>>>(vals, T, N, k, ids, out);
+  topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(vals, T, N, k, ids, out);
   return cudaGetLastError();
 }
 
