@@ -13,13 +13,16 @@
 //        TANH2:  epilogue h = tanh(acc) -> H[seg rows, 128 features].
 //   phase-1 unit (seg, mt, s):    D[128 x n] = W2[e][mt*128 : +128, K_s] . H_seg[:, K_s]^T
 //        epilogue: slot[s][seg rows][mt*128 : +128] = D (f32), no waiting.
-//        The last split to land for (segment, m-tile, warp quarter) sums the
+//        The epilogue warp whose split lands last for (segment, m-tile, warp
+//        quarter) queues a task for this CTA's reducer warps, which sum the
 //        slots in the fixed order 0..S-1 into slot 0 -- bit-reproducible
-//        without float atomics -- and the last segment to finish a column
-//        slice applies the combine (simulator.py:101-112) for its 32
+//        without float atomics -- and, for the last segment to finish a
+//        column slice, apply the combine (simulator.py:101-112) for its 32
 //        columns: out[t] = hidden[t] + sum_j w_tj * Y[row_tj], experts
-//        ascending.  Nothing on the streaming path ever blocks on another CTA
-//        except phase-1 loads of H (which queue order makes ready).
+//        ascending.  Nothing on the streaming path blocks on another CTA
+//        except phase-1 loads of H (which queue order makes ready), and no
+//        latency-bound L2 traffic sits in the epilogue (measured: doing the
+//        reductions in the epilogue under a saturated HBM cost 2x).
 //
 // Swap-AB: weight rows are the MMA M (=128) dimension, the segment's tokens
 // the MMA N dimension (16..256, rounded to 16), so decode streams each used
@@ -32,7 +35,8 @@
 // Warp roles (256 threads, one CTA per SM):
 //   warp 0      TMA producer + unit scheduler (one elected lane)
 //   warp 1      tcgen05.mma issuer (one lane)
-//   warp 2      TMEM allocator
+//   warp 2      TMEM allocator, then reducer
+//   warp 3      reducer (split-K sums + fused combine, fed by the epilogue)
 //   warps 4..7  epilogue: TMEM -> registers -> activation -> global
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -146,6 +150,59 @@ __device__ __noinline__ void combine_column(const FfnParams& p, int r) {
   }
 }
 
+// ------------------------------------------------ epilogue -> reducer tasks
+// Bounded MPMC ticket queue in shared memory (epilogue warps push, the two
+// reducer warps pop).  seq[i] == t: slot free for ticket t; == t + 1: task
+// of ticket t ready.
+constexpr int kTaskRing = 32;
+constexpr int kTaskReduce = 0, kTaskCombine = 1;
+
+struct TaskQueue {
+  int seq[kTaskRing];
+  int ring[kTaskRing];
+  int head, tail, epi_done;
+};
+
+__device__ __forceinline__ int make_task(int kind, int seg, int mt, int q) {
+  return (kind << 30) | (seg << 16) | (mt << 2) | q;
+}
+
+__device__ __forceinline__ int* seg_done_counter(const FfnParams& p, int mt, int q) {
+  return p.counters + 1 + p.max_seg + p.max_seg * p.tiles2 * 4 + mt * 4 + q;
+}
+
+__device__ __noinline__ void task_push(TaskQueue* q, int task) {
+  const int t = atomicAdd(&q->tail, 1);
+  volatile int* seq = q->seq;
+  Watchdog wd;
+  while (seq[t % kTaskRing] != t) {  // wait for the slot's previous lap to drain
+    __nanosleep(32);
+    wd.tick(10);
+  }
+  reinterpret_cast<volatile int*>(q->ring)[t % kTaskRing] = task;
+  __threadfence_block();
+  seq[t % kTaskRing] = t + 1;
+}
+
+// Returns -1 once every epilogue warp is done and the queue is drained.
+__device__ __noinline__ int task_pop(TaskQueue* q) {
+  const int h = atomicAdd(&q->head, 1);
+  volatile int* seq = q->seq;
+  volatile int* vq = reinterpret_cast<volatile int*>(q);
+  while (true) {
+    if (seq[h % kTaskRing] == h + 1) {
+      __threadfence_block();
+      const int task = reinterpret_cast<volatile int*>(q->ring)[h % kTaskRing];
+      seq[h % kTaskRing] = h + kTaskRing;
+      return task;
+    }
+    const int done = vq[offsetof(TaskQueue, epi_done) / 4];
+    const int tail = vq[offsetof(TaskQueue, tail) / 4];
+    if (done == 4 && h >= tail) return -1;
+    __nanosleep(64);
+  }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_constant__ FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -162,9 +219,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   uint64_t* uempty = ufull + kUnitRing;
   int* uring = reinterpret_cast<int*>(uempty + kUnitRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
+  TaskQueue* tq = reinterpret_cast<TaskQueue*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < kTaskRing) tq->seq[threadIdx.x] = threadIdx.x;
   if (threadIdx.x == 0) {
+    tq->head = 0;
+    tq->tail = 0;
+    tq->epi_done = 0;
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -360,26 +422,20 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         if (lane == 0) mbar_arrive(&tempty[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
+        // Publish the slot; whoever completes a reduction hands the
+        // latency-bound follow-up (split sum, combine) to the reducer warps
+        // so this warp is back on TMEM without waiting on L2.
         __threadfence();
         __syncwarp();
-        int last = 1;
-        if (p.split2 > 1) {
-          int* cnt = p.counters + 1 + p.max_seg + (U.seg * p.tiles2 + U.mt) * 4 + q;
-          if (lane == 0) last = atom_add_acq_rel_gpu(cnt, 1) == p.split2 - 1;
-          last = __shfl_sync(0xffffffffu, last, 0);
-          if (!last) continue;
-          fence_acq_rel_gpu();
-          if (rv) reduce_splits(p, U.row0, U.n, r);
-          __threadfence();
-          __syncwarp();
+        if (lane == 0) {
+          if (p.split2 > 1) {
+            int* cnt = p.counters + 1 + p.max_seg + (U.seg * p.tiles2 + U.mt) * 4 + q;
+            if (atom_add_acq_rel_gpu(cnt, 1) == p.split2 - 1) task_push(tq, make_task(kTaskReduce, U.seg, U.mt, q));
+          } else if (atom_add_acq_rel_gpu(seg_done_counter(p, U.mt, q), 1) == nseg - 1) {
+            task_push(tq, make_task(kTaskCombine, 0, U.mt, q));
+          }
         }
-        int* done = p.counters + 1 + p.max_seg + p.max_seg * p.tiles2 * 4 + U.mt * 4 + q;
-        if (lane == 0) last = atom_add_acq_rel_gpu(done, 1) == nseg - 1;
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last && rv) {
-          fence_acq_rel_gpu();
-          combine_column(p, r);
-        }
+        __syncwarp();
         continue;
       }
       tc_fence_before();
@@ -392,6 +448,32 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
+    }
+    if (lane == 0) atomicAdd(&tq->epi_done, 1);
+  } else if (warp == 2 || warp == 3) {
+    // -------------------------------------------------- reducers
+    // Split-K sums and the final combine are chains of dependent L2 loads;
+    // with HBM saturated by the weight stream their latency is long, so
+    // they run here, overlapped with streaming, never in the epilogue.
+    while (true) {
+      int task = 0;
+      if (lane == 0) task = task_pop(tq);
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task < 0) break;
+      const int kind = task >> 30, seg = (task >> 16) & 0x3FFF, mt = (task >> 2) & 0x3FFF, q = task & 3;
+      const int r = mt * 128 + q * 32 + lane;
+      const bool rv = r < p.d;
+      fence_acq_rel_gpu();
+      int last = 1;
+      if (kind == kTaskReduce) {
+        if (rv) reduce_splits(p, p.seg_row[seg], p.seg_count[seg], r);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) last = atom_add_acq_rel_gpu(seg_done_counter(p, mt, q), 1) == nseg - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) fence_acq_rel_gpu();
+      }
+      if (last && rv) combine_column(p, r);
     }
   }
   tc_fence_before();
@@ -406,7 +488,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 template <int BN, int STAGES>
 static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s) {
   constexpr size_t smem =
-      1024 + STAGES * (kTileA + BN * 128) + (2 * STAGES + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
+      1024 + STAGES * (kTileA + BN * 128) + (2 * STAGES + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16 +
+      sizeof(TaskQueue);
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static int configured_device = -1;
   int dev = 0;
