@@ -42,30 +42,35 @@ def _newer(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    """Compile liblynx_b200.so; trace=True builds the diagnostic variant
+    liblynx_b200_trace.so (-DLYNX_TRACE: per-unit timeline records)."""
+    build_dir = os.path.join(BUILD, "trace") if trace else BUILD
+    lib_path = LIB.replace(".so", "_trace.so") if trace else LIB
+    extra = ["-DLYNX_TRACE"] if trace else []
+    os.makedirs(build_dir, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
     cc = nvcc()
     headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "lynx_b200.h")]
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _newer(obj, [path] + headers):
-            cmd = [cc, *ARCH, *FLAGS, "-I", INCLUDE, "-c", path, "-o", obj]
+            cmd = [cc, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _newer(LIB, objs):
-        tmp = LIB + ".tmp"
+    if force or _newer(lib_path, objs):
+        tmp = lib_path + ".tmp"
         cmd = [cc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-cudart", "static"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv))

@@ -13,7 +13,8 @@ import threading
 
 from .errors import NativeLibraryError, ValidationError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "liblynx_b200.so")
+LIB_PATH = os.environ.get(
+    "LYNX_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "liblynx_b200.so"))
 
 # include/lynx_b200.h constants
 LYNX_OK = 0

@@ -85,70 +85,139 @@ __device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u,
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.f + __expf(-g)) * u; }
 
+// Scalars and pointers the reducer paths need, copied once into registers:
+// reading FfnParams fields through a reference inside a non-inlined helper
+// turns every access into a generic load and serialises the load chain
+// (measured: ~1 L2 round trip per element).
+struct ReduceCtx {
+  float* __restrict__ partial;
+  const __nv_bfloat16* __restrict__ hidden;
+  const int32_t* __restrict__ tok_rows;
+  const float* __restrict__ tok_weight;
+  __nv_bfloat16* __restrict__ out_bf16;
+  float* __restrict__ out_f32;
+  size_t stride;  // one split slot: rows_cap * d floats
+  int d, split2, T, k;
+};
+
+__device__ __forceinline__ ReduceCtx reduce_ctx(const FfnParams& p) {
+  ReduceCtx c;
+  c.partial = p.partial;
+  c.hidden = reinterpret_cast<const __nv_bfloat16*>(p.hidden);
+  c.tok_rows = p.tok_rows;
+  c.tok_weight = p.tok_weight;
+  c.out_bf16 = reinterpret_cast<__nv_bfloat16*>(p.out_bf16);
+  c.out_f32 = p.out_f32;
+  c.stride = static_cast<size_t>(p.rows_cap) * p.d;
+  c.d = p.d;
+  c.split2 = p.split2;
+  c.T = p.T;
+  c.k = p.k;
+  return c;
+}
+
 // slot0[row][r] = ((slot0 + slot1) + slot2) + ... for the segment's rows:
-// split-K partials summed in a fixed order (bit-reproducible).
-__device__ __noinline__ void reduce_splits(const FfnParams& p, int row0, int n, int r) {
-  const size_t stride = static_cast<size_t>(p.rows_cap) * p.d;
-  float* base = p.partial + static_cast<size_t>(row0) * p.d + r;
+// split-K partials summed in a fixed order (bit-reproducible).  Loads use
+// clamped in-bounds addresses so they issue unconditionally (64 in flight).
+__device__ __noinline__ void reduce_splits(const ReduceCtx c, int row0, int n, int r, bool rv) {
+  float* base = c.partial + static_cast<size_t>(row0) * c.d + r;
   for (int t0 = 0; t0 < n; t0 += 8) {
     float acc[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] = t0 + u < n ? __ldcg(base + static_cast<size_t>(t0 + u) * p.d) : 0.f;
-    for (int s0 = 1; s0 < p.split2; s0 += 8) {
-      float v[8][8];  // 64 independent loads in flight
+    for (int u = 0; u < 8; ++u) acc[u] = __ldcg(base + static_cast<size_t>(min(t0 + u, n - 1)) * c.d);
+    for (int s0 = 1; s0 < c.split2; s0 += 8) {
+      float v[8][8];
 #pragma unroll
       for (int s = 0; s < 8; ++s)
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          v[s][u] = (s0 + s < p.split2 && t0 + u < n)
-                        ? __ldcg(base + (s0 + s) * stride + static_cast<size_t>(t0 + u) * p.d)
-                        : 0.f;
+          v[s][u] = __ldcg(base + min(s0 + s, c.split2 - 1) * c.stride +
+                           static_cast<size_t>(min(t0 + u, n - 1)) * c.d);
 #pragma unroll
       for (int s = 0; s < 8; ++s)
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (s0 + s < p.split2) acc[u] += v[s][u];
+          if (s0 + s < c.split2) acc[u] += v[s][u];
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (t0 + u < n) __stcg(base + static_cast<size_t>(t0 + u) * p.d, acc[u]);
+      if (rv && t0 + u < n) __stcg(base + static_cast<size_t>(t0 + u) * c.d, acc[u]);
   }
 }
 
 // Combine for one output column r (all tokens): residual + experts in
 // ascending order, the reference's accumulation order (simulator.py:101-112).
-__device__ __noinline__ void combine_column(const FfnParams& p, int r) {
-  const float* Y = p.partial + r;
-  const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(p.hidden);
-  for (int t0 = 0; t0 < p.T; t0 += 8) {
-    float acc[8], y[8][LYNX_MAX_TOPK], w[8][LYNX_MAX_TOPK];
+// Token rows/weights are fetched lane-parallel (lane = token) and broadcast.
+// Called by all 32 lanes of a warp (r clamped in bounds, rv = column valid).
+__device__ __noinline__ void combine_column(const ReduceCtx c, int r, bool rv) {
+  const float* Y = c.partial + r;
+  const int lane = threadIdx.x & 31;
+  for (int t0 = 0; t0 < c.T; t0 += 32) {
+    int rows[LYNX_MAX_TOPK];
+    float wts[LYNX_MAX_TOPK];
+    const int tl = min(t0 + lane, c.T - 1);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int t = t0 + u;
-      acc[u] = (t < p.T && X) ? __bfloat162float(X[static_cast<size_t>(t) * p.d + r]) : 0.f;
-#pragma unroll
-      for (int j = 0; j < LYNX_MAX_TOPK; ++j) {
-        const int row = (t < p.T && j < p.k) ? p.tok_rows[t * p.k + j] : -1;
-        w[u][j] = row >= 0 ? p.tok_weight[t * p.k + j] : 0.f;
-        y[u][j] = row >= 0 ? __ldcg(Y + static_cast<size_t>(row) * p.d) : 0.f;
-      }
+    for (int j = 0; j < LYNX_MAX_TOPK; ++j) {
+      const int jj = min(j, c.k - 1);
+      const int row = c.tok_rows[tl * c.k + jj];
+      rows[j] = j < c.k ? row : -1;
+      wts[j] = c.tok_weight[tl * c.k + jj];
     }
+    const int tn = min(32, c.T - t0);
+    for (int u0 = 0; u0 < tn; u0 += 8) {
+      float acc[8], y[8][LYNX_MAX_TOPK], w[8][LYNX_MAX_TOPK];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 8; ++u) {
+        const int src = min(u0 + u, tn - 1);
+        const int t = t0 + src;
+        acc[u] = c.hidden ? __bfloat162float(c.hidden[static_cast<size_t>(t) * c.d + r]) : 0.f;
 #pragma unroll
-      for (int j = 0; j < LYNX_MAX_TOPK; ++j) acc[u] += w[u][j] * y[u][j];  // rows are -1-padded at the end
+        for (int j = 0; j < LYNX_MAX_TOPK; ++j) {
+          const int row = __shfl_sync(0xffffffffu, rows[j], src);
+          w[u][j] = row >= 0 ? __shfl_sync(0xffffffffu, wts[j], src) : 0.f;
+          y[u][j] = __ldcg(Y + static_cast<size_t>(max(row, 0)) * c.d);
+        }
+      }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int t = t0 + u;
-      if (t >= p.T) break;
-      const size_t o = static_cast<size_t>(t) * p.d + r;
-      if (p.out_f32)
-        p.out_f32[o] = acc[u];
-      else
-        reinterpret_cast<__nv_bfloat16*>(p.out_bf16)[o] = __float2bfloat16_rn(acc[u]);
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int j = 0; j < LYNX_MAX_TOPK; ++j)
+          if (j < c.k) acc[u] += w[u][j] * y[u][j];  // -1 rows carry weight 0
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u0 + u >= tn || !rv) break;
+        const size_t o = static_cast<size_t>(t0 + u0 + u) * c.d + r;
+        if (c.out_f32)
+          c.out_f32[o] = acc[u];
+        else
+          c.out_bf16[o] = __float2bfloat16_rn(acc[u]);
+      }
     }
   }
 }
+
+// ------------------------------------------------ optional timeline trace
+// Built only into the diagnostic library (-DLYNX_TRACE): one record per
+// unit / task with globaltimer start and end, read back by
+// lynx_debug_trace().  The production library compiles these to nothing.
+#ifdef LYNX_TRACE
+__device__ unsigned long long g_trace[4 * 65536];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace(int role, int id, uint64_t t0, uint64_t t1) {
+  const unsigned i = atomicAdd(&g_trace_n, 1u);
+  if (i < 65536) {
+    g_trace[4 * i + 0] = (static_cast<unsigned long long>(blockIdx.x) << 32) | static_cast<unsigned>(role);
+    g_trace[4 * i + 1] = static_cast<unsigned long long>(id);
+    g_trace[4 * i + 2] = t0;
+    g_trace[4 * i + 3] = t1;
+  }
+}
+#define LYNX_TRACE_T0 const uint64_t trace_t0 = globaltimer()
+#define LYNX_TRACE_REC(role, id) trace((role), (id), trace_t0, globaltimer())
+#else
+#define LYNX_TRACE_T0 (void)0
+#define LYNX_TRACE_REC(role, id) (void)0
+#endif
 
 // ------------------------------------------------ epilogue -> reducer tasks
 // Bounded MPMC ticket queue in shared memory (epilogue warps push, the two
@@ -254,6 +323,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   // Everything above overlapped the previous kernel (programmatic launch);
   // the dispatch plan and gathered rows are only read after this point.
   griddep_wait();
+#ifdef LYNX_TRACE
+  const uint64_t cta_t0 = globaltimer();
+#endif
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
   const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
@@ -261,7 +333,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
     // No token routed here (an expert-parallel shard can receive none):
     // the output is the residual (or zeros for a partial).
     if (warp >= 4)
-      for (int r = blockIdx.x * 128 + (threadIdx.x - 128); r < p.d; r += gridDim.x * 128) combine_column(p, r);
+      for (int r0 = blockIdx.x * 128 + (warp - 4) * 32; r0 < p.d; r0 += gridDim.x * 128)
+        combine_column(reduce_ctx(p), min(r0 + lane, p.d - 1), r0 + lane < p.d);
   }
 
   if (warp == 0) {
@@ -286,6 +359,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         const CUtensorMap* ma = U.phase == 0 ? &p.map_w1 : &p.map_w2;
         const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
         if (U.phase == 1) {
+          LYNX_TRACE_T0;
           const int* done = p.counters + 1 + U.seg;
           Watchdog wd;
           while (ld_acquire_gpu(done) < 4 * p.tiles1) {
@@ -293,6 +367,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
             wd.tick(2);
           }
           fence_proxy_async();  // H was written by generic stores; TMA reads it
+          LYNX_TRACE_REC(1, u);
         }
         const int nb = U.nmma >> 4;
         const uint32_t bytes = kTileA + nb * kBoxB;
@@ -326,6 +401,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         if (!decode_unit(p, nseg, u, U)) break;
         const uint32_t idesc = idesc_bf16_f32(128, U.nmma);
         mbar_wait(&tempty[acc], aphase ^ 1, 5);
+        LYNX_TRACE_T0;
         tc_fence_after();
         const uint32_t dt = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
@@ -343,6 +419,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           }
         }
         umma_commit(&tfull[acc]);
+        LYNX_TRACE_REC(4, u);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
@@ -364,6 +441,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       Unit U;
       if (!decode_unit(p, nseg, u, U)) break;
       mbar_wait(&tfull[acc], aphase, 8);
+      LYNX_TRACE_T0;
       tc_fence_after();
       const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
       if (U.phase == 0) {
@@ -436,6 +514,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           }
         }
         __syncwarp();
+        if (lane == 0) LYNX_TRACE_REC(2, u);
         continue;
       }
       tc_fence_before();
@@ -446,6 +525,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
+      if (lane == 0) LYNX_TRACE_REC(2, u);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
@@ -455,29 +535,36 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
     // Split-K sums and the final combine are chains of dependent L2 loads;
     // with HBM saturated by the weight stream their latency is long, so
     // they run here, overlapped with streaming, never in the epilogue.
+    const ReduceCtx ctx = reduce_ctx(p);
     while (true) {
       int task = 0;
       if (lane == 0) task = task_pop(tq);
       task = __shfl_sync(0xffffffffu, task, 0);
       if (task < 0) break;
+      LYNX_TRACE_T0;
       const int kind = task >> 30, seg = (task >> 16) & 0x3FFF, mt = (task >> 2) & 0x3FFF, q = task & 3;
       const int r = mt * 128 + q * 32 + lane;
       const bool rv = r < p.d;
       fence_acq_rel_gpu();
       int last = 1;
       if (kind == kTaskReduce) {
-        if (rv) reduce_splits(p, p.seg_row[seg], p.seg_count[seg], r);
+        reduce_splits(ctx, p.seg_row[seg], p.seg_count[seg], min(r, p.d - 1), rv);
         __threadfence();
         __syncwarp();
         if (lane == 0) last = atom_add_acq_rel_gpu(seg_done_counter(p, mt, q), 1) == nseg - 1;
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) fence_acq_rel_gpu();
       }
-      if (last && rv) combine_column(p, r);
+      if (last) combine_column(ctx, min(r, p.d - 1), rv);
+      __syncwarp();
+      if (lane == 0) LYNX_TRACE_REC(last ? 6 : 3, task);
     }
   }
   tc_fence_before();
   __syncthreads();
+#ifdef LYNX_TRACE
+  if (threadIdx.x == 0) trace(5, nseg, cta_t0, globaltimer());
+#endif
   griddep_launch_dependents();
   if (warp == 2) {
     tc_fence_after();
@@ -517,3 +604,17 @@ cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s)
 }
 
 }  // namespace lynx
+
+#ifdef LYNX_TRACE
+// Diagnostic library only: copy out and reset the timeline trace.
+extern "C" int lynx_debug_trace(unsigned long long* host, int max_records) {
+  unsigned n = 0;
+  if (cudaMemcpyFromSymbol(&n, lynx::g_trace_n, sizeof(n)) != cudaSuccess) return -1;
+  if (n > 65536u) n = 65536u;
+  if (static_cast<int>(n) > max_records) n = static_cast<unsigned>(max_records);
+  if (n && cudaMemcpyFromSymbol(host, lynx::g_trace, n * 4 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  unsigned z = 0;
+  cudaMemcpyToSymbol(lynx::g_trace_n, &z, sizeof(z));
+  return static_cast<int>(n);
+}
+#endif
