@@ -151,9 +151,8 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.perm_weight = take(sizeof(float) * c.rows_cap);
   p.tok_rows = take(sizeof(int32_t) * T * k);
   p.tok_weight = take(sizeof(float) * T * k);
-  // ticket + phase-0 done per segment + splits landed per (segment, m-tile,
-  // warp quarter) + segments done per (m-tile, warp quarter)
-  p.n_counters = 1 + c.max_seg + c.max_seg * g.tiles2 * 4 + g.tiles2 * 4;
+  // unit ticket + phase-0 tiles published per segment
+  p.n_counters = 1 + c.max_seg;
   p.counters = take(sizeof(int32_t) * p.n_counters);
   p.x_perm = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * d);
   p.h = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * ff);
@@ -227,7 +226,7 @@ inline void record(cudaEvent_t const* ev, int i, cudaStream_t s) {
 }
 
 // K2 gather -> K3 expert GEMM + combine, on a plan already in the workspace.
-// ev (optional): [0] before K2, [1] before K3, [2] after K3.
+// ev (optional): [0] before K2 (gather), [1] before K3 (FFN), [2] before K4 (combine).
 int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_t* out_bf16, float* out_f32,
                    void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev) {
   const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
@@ -267,7 +266,6 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.h = at<uint16_t>(ws, P.h);
   fp.partial = at<float>(ws, P.y);
   fp.counters = o.counters;
-  fp.max_seg = c.max_seg;
   fp.d = d;
   fp.ff = ff;
   fp.act = L->activation;
@@ -278,17 +276,24 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.kb2_per = g.kb2_per;
   fp.kb2_total = g.kb2_total;
   fp.rows_cap = c.rows_cap;
-  fp.T = T;
-  fp.k = k;
-  fp.hidden = out_f32 ? nullptr : hidden;
-  fp.tok_rows = o.tok_rows;
-  fp.tok_weight = o.tok_weight;
-  fp.out_bf16 = out_bf16;
-  fp.out_f32 = out_f32;
   record(ev, 1, s);
   st = cuda_status(launch_ffn(fp, g.bn, sms, s));
+  if (st) return st;
+
+  CombineArgs ca;
+  ca.hidden = out_f32 ? nullptr : hidden;
+  ca.partial = fp.partial;
+  ca.slot_stride = static_cast<size_t>(c.rows_cap) * d;
+  ca.split2 = g.split2;
+  ca.T = T;
+  ca.k = k;
+  ca.d = d;
+  ca.tok_rows = o.tok_rows;
+  ca.tok_weight = o.tok_weight;
+  ca.out_bf16 = out_bf16;
+  ca.out_f32 = out_f32;
   record(ev, 2, s);
-  return st;
+  return cuda_status(launch_combine(ca, s));
 }
 
 void* aligned_ws(void* ws) {

@@ -39,6 +39,79 @@ cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
   return launch_pdl(gather_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, s, a);
 }
 
+// ------------------------------------------------------------------- K4
+// out[t] = hidden[t] + sum_j w_tj * (slot0 + slot1 + ... + slot_{S-1})[row_tj],
+// j over the token's experts ascending and s in order: the reference's
+// accumulation order (simulator.py:101-112) with a fixed split-K order, so
+// the layer output is bit-reproducible.  One CTA per (token, 512 columns);
+// the token's rows are staged once, then all k*S float4 loads issue together.
+__global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
+  __shared__ int s_rows[LYNX_MAX_TOPK];
+  __shared__ float s_w[LYNX_MAX_TOPK];
+  griddep_launch_dependents();
+  griddep_wait();  // partial slots come from K3
+  const int t = blockIdx.y;
+  if (threadIdx.x < a.k) {
+    s_rows[threadIdx.x] = a.tok_rows[t * a.k + threadIdx.x];
+    s_w[threadIdx.x] = a.tok_weight[t * a.k + threadIdx.x];
+  }
+  __syncthreads();
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c >= a.d) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.hidden) {
+    const __nv_bfloat162* h =
+        reinterpret_cast<const __nv_bfloat162*>(a.hidden + static_cast<size_t>(t) * a.d + c);
+    const float2 h0 = __bfloat1622float2(h[0]), h1 = __bfloat1622float2(h[1]);
+    acc = make_float4(h0.x, h0.y, h1.x, h1.y);
+  }
+  const int n = a.k * a.split2;
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < n; i0 += 16) {
+    float4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = min(i0 + u, n - 1);
+      const int j = i / a.split2, s = i - j * a.split2;
+      const int row = max(s_rows[j], 0);
+      v[u] = *reinterpret_cast<const float4*>(a.partial + s * a.slot_stride + static_cast<size_t>(row) * a.d + c);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = i0 + u;
+      if (i >= n) break;
+      const int j = i / a.split2, s = i - j * a.split2;
+      if (s == 0) {
+        y = v[u];
+      } else {
+        y.x += v[u].x;
+        y.y += v[u].y;
+        y.z += v[u].z;
+        y.w += v[u].w;
+      }
+      if (s == a.split2 - 1 && s_rows[j] >= 0) {
+        const float w = s_w[j];
+        acc.x += w * y.x;
+        acc.y += w * y.y;
+        acc.z += w * y.z;
+        acc.w += w * y.w;
+      }
+    }
+  }
+  const size_t o = static_cast<size_t>(t) * a.d + c;
+  if (a.out_f32) {
+    *reinterpret_cast<float4*>(a.out_f32 + o) = acc;
+  } else {
+    __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(a.out_bf16 + o);
+    out[0] = __floats2bfloat162_rn(acc.x, acc.y);
+    out[1] = __floats2bfloat162_rn(acc.z, acc.w);
+  }
+}
+
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s) {
+  return launch_pdl(combine_kernel, dim3((a.d + 511) / 512, a.T), dim3(128), 0, s, a);
+}
+
 // --------------------------------------------------------------- packing
 // w13 row r of expert e: tile = r/128, q = (r%128)/32, half = (r%32)/16,
 // i = r%16 -> feature f = 64*tile + 16*q + i of w1 (half 0) or w3 (half 1).

@@ -80,9 +80,7 @@ struct SelectArgs {
 };
 
 // Grouped expert FFN (K3).  Phase 0 = gate/up (or tanh w1) over d, phase 1 =
-// down projection over ff, split-K into `split2` partials; the last phase-1
-// unit of every 128-column m-tile reduces the partials and applies the
-// combine (+ residual) for that tile.
+// down projection over ff, split-K into `split2` partial slots that K4 sums.
 struct FfnParams {
   CUtensorMap map_w1;  // (d, rows1, E)   box (64, 128, 1)
   CUtensorMap map_w2;  // (ff, d, E)      box (64, 128, 1)
@@ -94,19 +92,22 @@ struct FfnParams {
   const int32_t* seg_count;
   uint16_t* h;      // [rows_cap, ff] bf16
   float* partial;   // [split2, rows_cap, d] f32
-  int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s,
-                    // [1 + max_seg + mt] phase-1 units done for m-tile mt
-  int max_seg;
+  int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s
   int d, ff, act;
   int tiles1, kb1;  // phase 0: 128-row tiles per segment, 64-wide k blocks
   int tiles2, split2, kb2_per, kb2_total;
   int rows_cap;
-  // fused combine (K4)
-  int T, k;
-  const uint16_t* hidden;   // residual; null -> no residual (EP partial)
+};
+
+// K4: split-K sum + weighted combine (+ residual).
+struct CombineArgs {
+  const uint16_t* hidden;  // residual; null -> no residual (EP partial)
+  const float* partial;    // [split2][rows_cap][d]
+  size_t slot_stride;      // rows_cap * d
+  int split2, T, k, d;
   const int32_t* tok_rows;
   const float* tok_weight;
-  uint16_t* out_bf16;
+  uint16_t* out_bf16;  // exactly one of the outputs is set
   float* out_f32;
 };
 
@@ -131,6 +132,7 @@ cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_poli
                         cudaStream_t s);
 cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s);
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s);
 cudaError_t launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,
                             cudaStream_t s);
 cudaError_t launch_ep_pack(const uint16_t* hidden_local, const int32_t* assigned, int T_local, int k, int N, int G,
