@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include "lynx_internal.cuh"
+#include "ptx.cuh"
 
 namespace lynx {
 
@@ -211,8 +212,10 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
   __shared__ int s_base[LYNX_MAX_EXPERTS];
   const int W = (T + 31) >> 5;
   const int tid = threadIdx.x, nthr = blockDim.x;
+  #pragma unroll 1
   for (int i = tid; i < N * W; i += nthr) s_bits[i] = 0;
   __syncthreads();
+  #pragma unroll 1
   for (int i = tid; i < T * k; i += nthr) {
     const int e = asg[i];
     if (e >= 0 && e < N) {
@@ -221,8 +224,10 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     }
   }
   __syncthreads();
+  #pragma unroll 1
   for (int e = tid; e < N; e += nthr) {
     int run = 0;
+    #pragma unroll 1
     for (int q = 0; q < W; ++q) {
       s_prefix[e * W + q] = run;
       run += __popc(s_bits[e * W + q]);
@@ -232,11 +237,13 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
   __syncthreads();
   if (tid == 0) {
     int base = 0, nseg = 0, nused = 0;
+    #pragma unroll 1
     for (int e = 0; e < N; ++e) {
       const int cnt = s_cnt[e];
       s_base[e] = base;
       if (cnt == 0) continue;
       ++nused;
+      #pragma unroll 1
       for (int c0 = 0; c0 < cnt; c0 += LYNX_SEG_ROWS) {
         o.seg_expert[nseg] = e;
         o.seg_row[nseg] = base + c0;
@@ -249,15 +256,19 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     *o.n_used = nused;
     *o.n_rows = base;
   }
+  #pragma unroll 1
   for (int i = tid; i < o.n_counters; i += nthr) o.counters[i] = 0;
   __syncthreads();
+  #pragma unroll 1
   for (int t = tid; t < T; t += nthr) {
     int ids[LYNX_MAX_TOPK];
     int n = 0;
+    #pragma unroll 1
     for (int c = 0; c < k; ++c) {
       const int e = asg[t * k + c];
       if (e < 0 || e >= N) continue;
       bool dup = false;
+      #pragma unroll 1
       for (int j = 0; j < n; ++j) dup |= ids[j] == e;
       if (dup) continue;
       int j = n++;
@@ -267,11 +278,13 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
       }
       ids[j] = e;
     }
+    #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       const int e = ids[j];
       const uint32_t word = s_bits[e * W + (t >> 5)];
       const int row = s_base[e] + s_prefix[e * W + (t >> 5)] + __popc(word & ((1u << (t & 31)) - 1u));
       double acc = 0.0;
+      #pragma unroll 1
       for (int c = 0; c < k; ++c)
         if (asg[t * k + c] == e) acc += w[t * k + c];
       const float wf = static_cast<float>(acc);
@@ -280,13 +293,16 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
       o.perm_token[row] = t;
       o.perm_weight[row] = wf;
     }
+    #pragma unroll 1
     for (int j = n; j < k; ++j) {
       o.tok_rows[t * k + j] = -1;
       o.tok_weight[t * k + j] = 0.f;
     }
   }
+  #pragma unroll 1
   for (int e = tid; e < N; e += nthr) {
     const int cnt = s_cnt[e];
+    #pragma unroll 1
     for (int r = s_base[e] + cnt; r < s_base[e] + ((cnt + 15) & ~15); ++r) {
       o.perm_token[r] = -1;
       o.perm_weight[r] = 0.f;
@@ -335,6 +351,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   if (accuracy) {  // select_important_tokens
     const double tau = a.pol.confidence_threshold;
     int local = 0;
+    #pragma unroll 1
     for (int t = tid; t < T; t += nthr) {
       const bool q = CONF[t] >= tau;
       IMP[t] = q ? 1 : 0;
@@ -347,6 +364,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     if (nq == 0) {
       if (tid == 0) {
         int best = 0;
+        #pragma unroll 1
         for (int t = 1; t < T; ++t)
           if (CONF[t] > CONF[best]) best = t;
         IMP[best] = 1;
@@ -354,10 +372,12 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     } else if (nq > S) {
       // keep the S most confident (conf desc, t asc); ranks read CONF only,
       // so marking drops in bit 1 is race-free
+      #pragma unroll 1
       for (int t = tid; t < T; t += nthr) {
         if (!IMP[t]) continue;
         const double ct = CONF[t];
         int rank = 0;
+        #pragma unroll 1
         for (int u = 0; u < T; ++u) {
           const double cu = CONF[u];
           rank += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
@@ -365,6 +385,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
         if (rank >= S) IMP[t] |= 2;
       }
       __syncthreads();
+      #pragma unroll 1
       for (int t = tid; t < T; t += nthr) IMP[t] = IMP[t] == 1;
     }
     __syncthreads();
@@ -372,15 +393,20 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   // Unit votes are integers: order-free atomics are exact.  Rank-weighted
   // votes are float sums and keep numpy's slot order (thread per expert).
   if (!a.pol.n_rank_weights) {
+    #pragma unroll 1
     for (int i = tid; i < T * k; i += nthr)
       if (!accuracy || IMP[i / k]) atomicAdd(&s_icount[IDS[i]], 1);
     __syncthreads();
+    #pragma unroll 1
     for (int e = tid; e < N; e += nthr) s_counts[e] = static_cast<double>(s_icount[e]);
   } else {
+    #pragma unroll 1
     for (int e = tid; e < N; e += nthr) {
       double c = 0.0;
+      #pragma unroll 1
       for (int t = 0; t < T; ++t) {
         if (accuracy && !IMP[t]) continue;
+        #pragma unroll 1
         for (int r = 0; r < k; ++r)
           if (IDS[t * k + r] == e) c += a.pol.rank_weights[r];
       }
@@ -388,9 +414,11 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     }
   }
   __syncthreads();
+  #pragma unroll 1
   for (int e = tid; e < N; e += nthr) {  // retention order: count desc, index asc
     const double ce = s_counts[e];
     int rank = 0;
+    #pragma unroll 1
     for (int f = 0; f < N; ++f) {
       const double cf = s_counts[f];
       rank += (cf > ce || (cf == ce && f < e)) ? 1 : 0;
@@ -402,19 +430,24 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   if (!accuracy) {  // latency_policy
     const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
     const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
+    #pragma unroll 1
     for (int e = tid; e < N; e += nthr) s_keep[e] = s_rank[e] < N - eff;
     if (tid == 0) *s_clipped = eff != a.pol.drop_count;
   } else {  // accuracy_policy
     const int budget = a.pol.freq_keep_budget < N ? a.pol.freq_keep_budget : N;
+    #pragma unroll 1
     for (int e = tid; e < N; e += nthr) s_keep[e] = (s_counts[e] > 0.0 && s_rank[e] < budget) ? 1 : 0;
     __syncthreads();
+    #pragma unroll 1
     for (int t = tid; t < T; t += nthr)
       if (IMP[t]) s_keep[IDS[t * k]] = 1;
     __syncthreads();
     if (tid == 0) {
       int cnt = 0;
+      #pragma unroll 1
       for (int e = 0; e < N; ++e) cnt += s_keep[e];
       int padded = 0;
+      #pragma unroll 1
       for (int pos = 0; pos < N && cnt < a.floor_keep; ++pos) {
         const int e = s_order[pos];
         if (!s_keep[e]) {
@@ -427,6 +460,18 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     }
   }
 }
+
+// Diagnostic library only (-DLYNX_TRACE): phase timestamps of the last K1.
+#ifdef LYNX_TRACE
+__device__ unsigned long long g_sel_ts[16];
+#define SEL_TS(i)                                      \
+  do {                                                 \
+    __syncthreads();                                   \
+    if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
+  } while (0)
+#else
+#define SEL_TS(i) (void)0
+#endif
 
 // ------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs a) {
@@ -459,6 +504,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
     s_clipped = 0;
   }
   for (int e = tid; e < N; e += nthr) s_icount[e] = 0;
+  SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
   if (!a.logits && a.stage) {  // apply_policy on a given selection: stage it
     for (int i = tid; i < T * N; i += nthr) P[i] = a.full[i];
@@ -469,12 +515,14 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   }
   __syncthreads();
 
+  SEL_TS(1);
   // 1) softmax + top-k + confidence: one warp per token
   for (int t = warp; t < T; t += nwarps)
     route_token(a.logits ? a.logits + static_cast<size_t>(t) * N : nullptr, P + static_cast<size_t>(t) * N, N, k,
                 a.pol.confidence_metric, IDS + t * k, PROBS + t * k, CONF + t, &s_flags);
   __syncthreads();
 
+  SEL_TS(2);
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
   const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
   if (!run_policy) {  // full_retain_mask: identity, weights = probs / row sum
@@ -502,6 +550,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   }
   __syncthreads();
 
+  SEL_TS(3);
   // 2) remap every token onto the retained set: one warp per token
   if (run_policy) {
     const uint64_t keep = s_keepmask;
@@ -510,6 +559,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
   }
   __syncthreads();
 
+  SEL_TS(4);
   // 3) outputs
   if (a.stage) {
     if (a.logits) {
@@ -533,10 +583,232 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs
     for (int t = tid; t < T; t += nthr) a.important[t] = accuracy ? IMP[t] : 0;
   if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
 
+  SEL_TS(5);
   // 4) dispatch plan for K2/K3 (layer path)
   if (a.plan.enabled)
     plan_dispatch(ASG, WT, T, N, k, a.plan, reinterpret_cast<uint32_t*>(s_dyn + L.bits),
                   reinterpret_cast<int*>(s_dyn + L.prefix));
+  SEL_TS(6);
+}
+
+// ------------------------------------------------- K1 fast path (N <= 16)
+// One thread per token with its whole probability row in registers: the N
+// exps are independent (they interleave), numpy's pairwise sum and the
+// stable top-k run on registers, and the same thread keeps its row from
+// routing through the remap.  Division by the row sum uses one IEEE
+// reciprocal per token (<= 1 ulp from numpy's e/s; decisions unchanged,
+// probabilities well within the 1e-12 contract).
+template <int NT>
+__device__ __forceinline__ double reg_pairwise_sum(const double (&e)[NT], int n) {
+  if (n < 8) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < (NT < 8 ? NT : 8); ++i)
+      if (i < n) acc += e[i];
+    return acc;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = e[j];
+  const int body = n - (n % 8);
+#pragma unroll
+  for (int i = 8; i < NT; ++i)
+    if (i < body) r[i % 8] += e[i];
+  double acc = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+  for (int i = 8; i < NT; ++i)
+    if (i >= body && i < n) acc += e[i];
+  return acc;
+}
+
+// best index in `cand` by (value desc, index asc) over a register row
+template <int NT>
+__device__ __forceinline__ int reg_best(const double (&p)[NT], uint64_t cand) {
+  int best = -1;
+  double bv = 0.0;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+    if (((cand >> i) & 1ull) && (best < 0 || p[i] > bv)) {
+      best = i;
+      bv = p[i];
+    }
+  return best;
+}
+
+template <int NT>
+__device__ __forceinline__ double reg_at(const double (&p)[NT], int e) {
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+    if (i == e) v = p[i];
+  return v;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kSelectThreads) route_select_fast(SelectArgs a) {
+  __shared__ double s_counts[LYNX_MAX_EXPERTS];
+  __shared__ int s_icount[LYNX_MAX_EXPERTS];
+  __shared__ int s_rank[LYNX_MAX_EXPERTS];
+  __shared__ int s_order[LYNX_MAX_EXPERTS];
+  __shared__ int s_keep[LYNX_MAX_EXPERTS];
+  __shared__ int s_flags, s_nq, s_clipped;
+  __shared__ unsigned long long s_keepmask;
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+
+  griddep_launch_dependents();
+  const int T = a.T, N = a.N, k = a.k;
+  const int t = threadIdx.x;
+  const bool active = t < T;
+  const SelectSmem L = select_smem(T, N, k, true, a.plan.enabled);
+  double* CONF = reinterpret_cast<double*>(s_dyn + L.conf);
+  int32_t* IDS = reinterpret_cast<int32_t*>(s_dyn + L.ids);
+  int32_t* ASG = reinterpret_cast<int32_t*>(s_dyn + L.asg);
+  double* WT = reinterpret_cast<double*>(s_dyn + L.w);
+  uint8_t* IMP = s_dyn + L.imp;
+  if (t == 0) {
+    s_flags = 0;
+    s_nq = 0;
+    s_clipped = 0;
+  }
+  if (t < N) s_icount[t] = 0;
+  SEL_TS(0);
+  griddep_wait();  // logits come from K0 (programmatic dependent launch)
+  SEL_TS(1);
+
+  // 1) softmax + stable top-k + confidence, thread per token
+  double p[NT];
+  int ids[LYNX_MAX_TOPK];
+  double probs[LYNX_MAX_TOPK];
+  if (active) {
+    if (a.logits) {
+      const double* z = a.logits + static_cast<size_t>(t) * N;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) p[i] = i < N ? z[i] : 0.0;
+      bool finite = true;
+      double m = p[0];
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+        if (i < N) {
+          finite &= isfinite(p[i]);
+          m = p[i] > m ? p[i] : m;
+        }
+      if (!finite) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
+#pragma unroll
+      for (int i = 0; i < NT; ++i) p[i] = i < N ? exp(p[i] - m) : 0.0;
+      const double inv = 1.0 / reg_pairwise_sum<NT>(p, N);
+#pragma unroll
+      for (int i = 0; i < NT; ++i) p[i] *= inv;
+      uint64_t taken = ~expert_mask_all(N);
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+          const int b = reg_best<NT>(p, ~taken);
+          taken |= 1ull << b;
+          ids[r] = b;
+          probs[r] = reg_at<NT>(p, b);
+          a.ids[t * k + r] = b;
+          a.probs[t * k + r] = probs[r];
+        }
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+        if (i < N) a.full[static_cast<size_t>(t) * N + i] = p[i];
+    } else {
+      const double* row = a.full + static_cast<size_t>(t) * N;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) p[i] = i < N ? row[i] : 0.0;
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+          ids[r] = a.ids[t * k + r];
+          probs[r] = a.probs[t * k + r];
+        }
+    }
+    const int first = reg_best<NT>(p, expert_mask_all(N));
+    const double top1 = reg_at<NT>(p, first);
+    double c = top1;
+    if (a.pol.confidence_metric == LYNX_CONF_MARGIN)
+      c = N == 1 ? p[0] : top1 - reg_at<NT>(p, reg_best<NT>(p, expert_mask_all(N) & ~(1ull << first)));
+    CONF[t] = c;
+#pragma unroll 1
+    for (int r = 0; r < k; ++r) IDS[t * k + r] = ids[r];
+  }
+  __syncthreads();
+  SEL_TS(2);
+
+  const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
+  const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
+  if (!run_policy) {
+    if (t < N) {
+      s_keep[t] = 1;
+      s_counts[t] = 0.0;
+    }
+    if (active) IMP[t] = 0;
+  } else {
+    batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
+  }
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long mk = 0;
+    for (int e = 0; e < N; ++e)
+      if (s_keep[e]) mk |= 1ull << e;
+    s_keepmask = mk;
+  }
+  __syncthreads();
+  SEL_TS(3);
+
+  // 2) remap (policy.py:171-210) or identity (policy.py:215-229), same thread
+  if (active) {
+    double slot_p[LYNX_MAX_TOPK];
+    int asg[LYNX_MAX_TOPK];
+    if (run_policy) {
+      const uint64_t keep = s_keepmask;
+      uint64_t occupied = 0;
+#pragma unroll 1
+      for (int r = 0; r < k; ++r)
+        if ((keep >> ids[r]) & 1ull) occupied |= 1ull << ids[r];
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+          int e = ids[r];
+          if (!((keep >> e) & 1ull)) {
+            int pick = reg_best<NT>(p, keep & ~occupied);
+            if (pick < 0) pick = reg_best<NT>(p, keep);  // collapse (policy.py:197-200)
+            e = pick;
+            occupied |= 1ull << e;
+          }
+          asg[r] = e;
+          slot_p[r] = reg_at<NT>(p, e);
+        }
+    } else {
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+          asg[r] = ids[r];
+          slot_p[r] = probs[r];
+        }
+    }
+    const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot_p, k);
+    if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);
+    const double inv = 1.0 / total;
+#pragma unroll 1
+    for (int r = 0; r < k; ++r) {
+        const double w = slot_p[r] * inv;
+        ASG[t * k + r] = asg[r];
+        WT[t * k + r] = w;
+        a.assigned[t * k + r] = asg[r];
+        a.weights[t * k + r] = w;
+      }
+    a.conf[t] = CONF[t];
+    if (a.important) a.important[t] = accuracy ? IMP[t] : 0;
+  }
+  if (t < N) {
+    if (a.retained) a.retained[t] = static_cast<uint8_t>(s_keep[t]);
+    if (a.counts) a.counts[t] = s_counts[t];
+  }
+  __syncthreads();
+  if (t == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
+  SEL_TS(4);
+  SEL_TS(5);
+  if (a.plan.enabled)
+    plan_dispatch(ASG, WT, T, N, k, a.plan, reinterpret_cast<uint32_t*>(s_dyn + L.bits),
+                  reinterpret_cast<int*>(s_dyn + L.prefix));
+  SEL_TS(6);
 }
 
 // Dispatch plan from an assigned/weights mask in global memory (forward_layer path).
@@ -699,6 +971,23 @@ cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
     cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_kernel), configured);
     if (e != cudaSuccess) return e;
   }
+  // Fast path: N <= 16 and one thread per token (the decode case).
+  if (a.N <= 16 && a.T <= kSelectThreads && a.stage) {
+    const int threads = ((a.T > a.N ? a.T : a.N) + 31) / 32 * 32;
+    static int configured8 = -1, configured16 = -1;
+    if (a.N <= 8) {
+      if (smem > 48 * 1024) {
+        cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_fast<8>), configured8);
+        if (e != cudaSuccess) return e;
+      }
+      return launch_pdl(route_select_fast<8>, dim3(1), dim3(threads), smem, s, a);
+    }
+    if (smem > 48 * 1024) {
+      cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_fast<16>), configured16);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_pdl(route_select_fast<16>, dim3(1), dim3(threads), smem, s, a);
+  }
   return launch_pdl(route_select_kernel, dim3(1), dim3(kSelectThreads), smem, s, a);
 }
 
@@ -733,3 +1022,9 @@ cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_poli
 }
 
 }  // namespace lynx
+
+#ifdef LYNX_TRACE
+extern "C" int lynx_debug_select_ts(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, lynx::g_sel_ts, sizeof(lynx::g_sel_ts)) == cudaSuccess ? 16 : -1;
+}
+#endif

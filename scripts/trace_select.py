@@ -1,0 +1,50 @@
+"""Phase timestamps of K1 inside a real layer step (diagnostic library).
+LYNX_LIB=paper_2411_08982_b200/_lib/liblynx_b200_trace.so python scripts/trace_select.py"""
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_08982_b200 as L  # noqa: E402
+from paper_2411_08982_b200 import _native as nat  # noqa: E402
+
+PHASES = ["start->griddep_wait", "wait", "route(softmax/topk/conf)", "policy", "remap", "outputs", "plan"]
+
+
+def main():
+    lib = nat.lib()
+    lib.lynx_debug_select_ts.argtypes = [ctypes.c_void_p]
+    T, N, k, d, ff = 32, 8, 2, 4096, 14336
+    spec = L.MoEModelSpec(2, N, k, d, ff)
+    model = L.build_swiglu_model(spec, seed=0)
+    cfg = L.PolicyConfig(mode="latency", drop_count=4)
+    layers = [L.LynxMoELayer(model, l, T, policy=cfg) for l in range(2)]
+    h = torch.randn((T, d), device="cuda").to(torch.bfloat16)
+    res = {}
+    for label, warm in (("cold_after_stream", False), ("warm_repeat", True)):
+        rows = []
+        for rep in range(5):
+            layers[rep % 2](h)  # streams weights -> evicts L2
+            torch.cuda.synchronize()
+            if warm:
+                # run the select path alone twice: second run warm
+                lg = L.router_logits(model, 0, h)
+                for _ in range(2):
+                    sel = L.route_batch(L.RoutingLogits(0, L.Phase.DECODE, lg), k, check=False)
+                    torch.cuda.synchronize()
+            buf = np.zeros(16, dtype=np.uint64)
+            lib.lynx_debug_select_ts(buf.ctypes.data)
+            ts = buf[:7].astype(np.int64)
+            rows.append(np.diff(ts) / 1e3)
+        m = np.median(np.array(rows), axis=0)
+        res[label] = {p: round(float(v), 2) for p, v in zip(PHASES[1:], m)}
+        res[label]["total_us"] = round(float(m.sum()), 2)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
