@@ -50,12 +50,22 @@ constexpr int kUnitRing = 4;
 constexpr int kTileA = 128 * 64 * 2;  // 128 weight rows x 64 bf16 (one 128B-swizzled k block)
 constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
 
+constexpr int kGatherRows = 8;        // rows of the permuted buffer per gather unit
+constexpr int kPhaseGather = 2;
+
 struct Unit {
   int phase, seg, mt, split, kb0, kb1, expert, row0, n, nmma;
 };
 
-__device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u, Unit& U) {
+// Queue order: [gather units][phase-0 units][phase-1 units].
+__device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int ngather, int u, Unit& U) {
   if (u < 0) return false;
+  if (u < ngather) {
+    U.phase = kPhaseGather;
+    U.mt = u;
+    return true;
+  }
+  u -= ngather;
   const int nA = nseg * p.tiles1;
   if (u < nA) {
     U.phase = 0;
@@ -158,7 +168,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 #endif
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
-  const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
+  const int ngather = (*p.n_rows + kGatherRows - 1) / kGatherRows;
+  const int total = ngather + nseg * (p.tiles1 + p.tiles2 * p.split2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -178,23 +189,44 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           uphase ^= 1;
         }
         Unit U;
-        if (!decode_unit(p, nseg, u, U)) break;
+        if (!decode_unit(p, nseg, ngather, u, U)) break;
+        if (U.phase == kPhaseGather) continue;  // done by the epilogue warps
         const CUtensorMap* ma = U.phase == 0 ? &p.map_w1 : &p.map_w2;
         const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
-        if (U.phase == 1) {
-          LYNX_TRACE_T0;
-          const int* done = p.counters + 1 + U.seg;
-          Watchdog wd;
-          while (ld_acquire_gpu(done) < 4 * p.tiles1) {
-            __nanosleep(100);
-            wd.tick(2);
-          }
-          fence_proxy_async();  // H was written by generic stores; TMA reads it
-          LYNX_TRACE_REC(1, u);
-        }
         const int nb = U.nmma >> 4;
         const uint32_t bytes = kTileA + nb * kBoxB;
-        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+        // Weight tiles never depend on earlier units: issue the first stages
+        // of them, then wait for the activations (gathered rows for phase 0,
+        // H for phase 1), then fill in the activation tiles.
+        const int npre = min(STAGES, U.kb1 - U.kb0);
+        const int stage0 = stage;
+        for (int i = 0; i < npre; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1, 3);
+          mbar_expect_tx(&full[stage], bytes);
+          tma_load_3d(sA + stage * kTileA, ma, &full[stage], (U.kb0 + i) * 64, U.mt * 128, U.expert, pol_w);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        {
+          LYNX_TRACE_T0;
+          const int* dep = U.phase == 0 ? p.counters + 1 + p.max_seg : p.counters + 1 + U.seg;
+          const int need = 4 * (U.phase == 0 ? ngather : p.tiles1);  // one release per epilogue warp
+          Watchdog wd;
+          while (ld_acquire_gpu(dep) < need) {
+            __nanosleep(64);
+            wd.tick(2);
+          }
+          fence_proxy_async();  // written by generic stores, read by TMA
+          LYNX_TRACE_REC(1, u);
+        }
+        for (int i = 0; i < npre; ++i) {
+          const int st = (stage0 + i) % STAGES;
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d(sB + st * kTileB + j * kBoxB, mb, &full[st], (U.kb0 + i) * 64, U.row0 + 16 * j, pol_act);
+        }
+        for (int kb = U.kb0 + npre; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
           mbar_expect_tx(&full[stage], bytes);
           tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
@@ -221,7 +253,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           uphase ^= 1;
         }
         Unit U;
-        if (!decode_unit(p, nseg, u, U)) break;
+        if (!decode_unit(p, nseg, ngather, u, U)) break;
+        if (U.phase == kPhaseGather) continue;
         const uint32_t idesc = idesc_bf16_f32(128, U.nmma);
         mbar_wait(&tempty[acc], aphase ^ 1, 5);
         LYNX_TRACE_T0;
@@ -262,7 +295,26 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         uphase ^= 1;
       }
       Unit U;
-      if (!decode_unit(p, nseg, u, U)) break;
+      if (!decode_unit(p, nseg, ngather, u, U)) break;
+      if (U.phase == kPhaseGather) {
+        // K2 fused: copy kGatherRows rows of hidden into the permuted buffer
+        // (padding rows zero), 16 B per lane, all 4 epilogue warps.
+        const int row_lo = U.mt * kGatherRows;
+        const int rows = min(kGatherRows, *p.n_rows - row_lo);
+        const int nvec = p.d >> 3;
+        const uint4* src = reinterpret_cast<const uint4*>(p.hidden);
+        uint4* dst = reinterpret_cast<uint4*>(p.x_perm) + static_cast<size_t>(row_lo) * nvec;
+        for (int i = q * 32 + lane; i < rows * nvec; i += 128) {
+          const int r = i / nvec, v = i - r * nvec;
+          const int t = p.perm_token[row_lo + r];
+          dst[i] = t >= 0 ? src[static_cast<size_t>(t) * nvec + v] : make_uint4(0, 0, 0, 0);
+        }
+        __threadfence();
+        fence_proxy_async();  // read back through TMA by phase-0 units
+        __syncwarp();
+        if (lane == 0) red_release_gpu_add(p.counters + 1 + p.max_seg, 1);
+        continue;
+      }
       mbar_wait(&tfull[acc], aphase, 8);
       LYNX_TRACE_T0;
       tc_fence_after();
