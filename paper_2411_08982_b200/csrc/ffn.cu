@@ -195,47 +195,61 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
         const int nb = U.nmma >> 4;
         const uint32_t bytes = kTileA + nb * kBoxB;
-        // Weight tiles never depend on earlier units: issue the first stages
-        // of them, then wait for the activations (gathered rows for phase 0,
-        // H for phase 1), then fill in the activation tiles.
-        const int npre = min(STAGES, U.kb1 - U.kb0);
-        const int stage0 = stage;
-        for (int i = 0; i < npre; ++i) {
+        // The activation tiles depend on earlier units (gathered rows for
+        // phase 0, H for phase 1); the weight tiles never do.  While the
+        // dependency is unmet, keep streaming weight tiles into free stages
+        // and defer their activation loads; issue the deferred ones as soon
+        // as it is met.  (Once met, stages get both loads together.)
+        const int* dep = U.phase == 0 ? p.counters + 1 + p.max_seg : p.counters + 1 + U.seg;
+        const int need = 4 * (U.phase == 0 ? ngather : p.tiles1);  // one release per epilogue warp
+        bool ready = ld_acquire_gpu(dep) >= need;
+        if (ready) fence_proxy_async();  // activations written by generic stores, read by TMA
+        int pend_first = -1, pend_stage = 0;  // deferred k blocks: [pend_first, kb)
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
           mbar_expect_tx(&full[stage], bytes);
-          tma_load_3d(sA + stage * kTileA, ma, &full[stage], (U.kb0 + i) * 64, U.mt * 128, U.expert, pol_w);
+          tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
+          if (!ready) {
+            if (pend_first < 0) {
+              pend_first = kb;
+              pend_stage = stage;
+            }
+            ready = ld_acquire_gpu(dep) >= need;
+            if (!ready && kb - pend_first + 1 == STAGES) {  // every stage waits on it: block
+              LYNX_TRACE_T0;
+              Watchdog wd;
+              while (ld_acquire_gpu(dep) < need) {
+                __nanosleep(64);
+                wd.tick(2);
+              }
+              ready = true;
+              LYNX_TRACE_REC(1, u);
+            }
+            if (ready) {
+              fence_proxy_async();
+              for (int k2 = pend_first, st = pend_stage; k2 <= kb; ++k2, st = st + 1 == STAGES ? 0 : st + 1)
+                for (int j = 0; j < nb; ++j)
+                  tma_load_2d(sB + st * kTileB + j * kBoxB, mb, &full[st], k2 * 64, U.row0 + 16 * j, pol_act);
+            }
+          } else {
+            for (int j = 0; j < nb; ++j)
+              tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        {
-          LYNX_TRACE_T0;
-          const int* dep = U.phase == 0 ? p.counters + 1 + p.max_seg : p.counters + 1 + U.seg;
-          const int need = 4 * (U.phase == 0 ? ngather : p.tiles1);  // one release per epilogue warp
+        if (!ready) {  // unit shorter than the ring and still waiting
           Watchdog wd;
           while (ld_acquire_gpu(dep) < need) {
             __nanosleep(64);
             wd.tick(2);
           }
-          fence_proxy_async();  // written by generic stores, read by TMA
-          LYNX_TRACE_REC(1, u);
-        }
-        for (int i = 0; i < npre; ++i) {
-          const int st = (stage0 + i) % STAGES;
-          for (int j = 0; j < nb; ++j)
-            tma_load_2d(sB + st * kTileB + j * kBoxB, mb, &full[st], (U.kb0 + i) * 64, U.row0 + 16 * j, pol_act);
-        }
-        for (int kb = U.kb0 + npre; kb < U.kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1, 3);
-          mbar_expect_tx(&full[stage], bytes);
-          tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
-          for (int j = 0; j < nb; ++j)
-            tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          fence_proxy_async();
+          for (int k2 = pend_first, st = pend_stage; k2 < U.kb1; ++k2, st = st + 1 == STAGES ? 0 : st + 1)
+            for (int j = 0; j < nb; ++j)
+              tma_load_2d(sB + st * kTileB + j * kBoxB, mb, &full[st], k2 * 64, U.row0 + 16 * j, pol_act);
         }
       }
     }
