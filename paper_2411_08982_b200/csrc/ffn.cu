@@ -50,7 +50,7 @@ constexpr int kUnitRing = 4;
 constexpr int kTileA = 128 * 64 * 2;  // 128 weight rows x 64 bf16 (one 128B-swizzled k block)
 constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
 
-constexpr int kGatherRows = 8;        // rows of the permuted buffer per gather unit
+constexpr int kGatherRows = 1;        // rows of the permuted buffer per gather unit
 constexpr int kPhaseGather = 2;
 
 struct Unit {
@@ -311,17 +311,24 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       Unit U;
       if (!decode_unit(p, nseg, ngather, u, U)) break;
       if (U.phase == kPhaseGather) {
-        // K2 fused: copy kGatherRows rows of hidden into the permuted buffer
-        // (padding rows zero), 16 B per lane, all 4 epilogue warps.
-        const int row_lo = U.mt * kGatherRows;
-        const int rows = min(kGatherRows, *p.n_rows - row_lo);
+        // K2 fused: copy one row of hidden into the permuted buffer (padding
+        // rows zero) with all 4 epilogue warps; the loads of the row are
+        // independent (one memory round trip after the token lookup).
+        const int row = U.mt;
         const int nvec = p.d >> 3;
-        const uint4* src = reinterpret_cast<const uint4*>(p.hidden);
-        uint4* dst = reinterpret_cast<uint4*>(p.x_perm) + static_cast<size_t>(row_lo) * nvec;
-        for (int i = q * 32 + lane; i < rows * nvec; i += 128) {
-          const int r = i / nvec, v = i - r * nvec;
-          const int t = p.perm_token[row_lo + r];
-          dst[i] = t >= 0 ? src[static_cast<size_t>(t) * nvec + v] : make_uint4(0, 0, 0, 0);
+        const int t = p.perm_token[row];
+        const uint4* src = reinterpret_cast<const uint4*>(p.hidden) + static_cast<size_t>(t < 0 ? 0 : t) * nvec;
+        uint4* dst = reinterpret_cast<uint4*>(p.x_perm) + static_cast<size_t>(row) * nvec;
+        for (int i0 = q * 32 + lane; i0 < nvec; i0 += 128 * 4) {
+          uint4 v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int i = i0 + j * 128;
+            v[j] = (i < nvec && t >= 0) ? src[i] : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i0 + j * 128 < nvec) dst[i0 + j * 128] = v[j];
         }
         __threadfence();
         fence_proxy_async();  // read back through TMA by phase-0 units
