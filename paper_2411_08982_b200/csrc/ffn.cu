@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       const uint64_t pol_act = policy_evict_last();
       int stage = 0, slot = 0;
       uint32_t phase = 0, uphase = 0;
+      uint64_t known_ready = 0;  // bit 0: gather done; bit 1+s: H of segment s published
       while (true) {
         int u = atomicAdd(&p.counters[0], 1);
         if (u >= total) u = -1;
@@ -202,8 +203,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         // as it is met.  (Once met, stages get both loads together.)
         const int* dep = U.phase == 0 ? p.counters + 1 + p.max_seg : p.counters + 1 + U.seg;
         const int need = 4 * (U.phase == 0 ? ngather : p.tiles1);  // one release per epilogue warp
-        bool ready = ld_acquire_gpu(dep) >= need;
-        if (ready) fence_proxy_async();  // activations written by generic stores, read by TMA
+        // Readiness is sticky: remember it so each dependency costs one
+        // acquire load per CTA (an L2 round trip under a saturated HBM is ~1 us).
+        const uint64_t dep_bit = U.phase == 0 ? 1ull : (U.seg < 63 ? 2ull << U.seg : 0ull);
+        bool ready = (known_ready & dep_bit) != 0;
+        if (!ready && ld_acquire_gpu(dep) >= need) {
+          ready = true;
+          fence_proxy_async();  // activations written by generic stores, read by TMA
+        }
+        if (ready) known_ready |= dep_bit;
         int pend_first = -1, pend_stage = 0;  // deferred k blocks: [pend_first, kb)
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
@@ -226,6 +234,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
               LYNX_TRACE_REC(1, u);
             }
             if (ready) {
+              known_ready |= dep_bit;
               fence_proxy_async();
               for (int k2 = pend_first, st = pend_stage; k2 <= kb; ++k2, st = st + 1 == STAGES ? 0 : st + 1)
                 for (int j = 0; j < nb; ++j)
@@ -246,6 +255,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
             __nanosleep(64);
             wd.tick(2);
           }
+          known_ready |= dep_bit;
           fence_proxy_async();
           for (int k2 = pend_first, st = pend_stage; k2 < U.kb1; ++k2, st = st + 1 == STAGES ? 0 : st + 1)
             for (int j = 0; j < nb; ++j)
