@@ -42,23 +42,30 @@ def _newer(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, trace: bool = False, src_dir: str | None = None,
+          out: str | None = None) -> str:
     """Compile liblynx_b200.so; trace=True builds the diagnostic variant
-    liblynx_b200_trace.so (-DLYNX_TRACE: per-unit timeline records)."""
+    liblynx_b200_trace.so (-DLYNX_TRACE: per-unit timeline records).
+    src_dir/out build another source tree (A/B experiments) into `out`."""
     build_dir = os.path.join(BUILD, "trace") if trace else BUILD
     lib_path = LIB.replace(".so", "_trace.so") if trace else LIB
     extra = ["-DLYNX_TRACE"] if trace else []
+    csrc, inc = CSRC, INCLUDE
+    if src_dir is not None:
+        csrc, inc = os.path.join(src_dir, "paper_2411_08982_b200", "csrc"), os.path.join(src_dir, "include")
+        build_dir = os.path.join(BUILD, "ab_" + os.path.basename(out).replace(".so", ""))
+        lib_path = out
     os.makedirs(build_dir, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
     cc = nvcc()
-    headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "lynx_b200.h")]
+    headers = [os.path.join(csrc, h) for h in HEADERS] + [os.path.join(inc, "lynx_b200.h")]
     objs = []
     for src in SOURCES:
-        path = os.path.join(CSRC, src)
+        path = os.path.join(csrc, src)
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _newer(obj, [path] + headers):
-            cmd = [cc, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-c", path, "-o", obj]
+            cmd = [cc, *ARCH, *FLAGS, *extra, "-I", inc, "-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
@@ -73,4 +80,12 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv))
+    if "--ab" in sys.argv:  # python -m paper_2411_08982_b200._build --ab <git-rev> <out.so>
+        import tempfile
+        rev, out = sys.argv[sys.argv.index("--ab") + 1], os.path.abspath(sys.argv[sys.argv.index("--ab") + 2])
+        with tempfile.TemporaryDirectory() as tmp:
+            subprocess.run(f"git -C {ROOT} archive {rev} paper_2411_08982_b200/csrc include | tar -x -C {tmp}",
+                           shell=True, check=True)
+            print(build(verbose=True, force=True, src_dir=tmp, out=out))
+    else:
+        print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv))

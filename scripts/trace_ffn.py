@@ -1,6 +1,5 @@
 """Timeline of one FFN launch from the diagnostic library (LYNX_TRACE).
 Run:  LYNX_LIB=paper_2411_08982_b200/_lib/liblynx_b200_trace.so python scripts/trace_ffn.py"""
-import collections
 import ctypes
 import json
 import os
@@ -13,7 +12,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_08982_b200 as L  # noqa: E402
 from paper_2411_08982_b200 import _native as nat  # noqa: E402
 
-ROLES = {1: "h_wait", 2: "epilogue_unit", 3: "reduce_task", 4: "mma_unit", 5: "cta", 6: "reduce+combine_task"}
+ROLES = {1: "dep_wait", 2: "epilogue_unit", 4: "mma_unit", 5: "cta"}
+
+
+def stats(x):
+    x = np.asarray(x, dtype=np.float64)
+    if x.size == 0:
+        return None
+    return {"n": int(x.size), "mean": round(float(x.mean()), 2), "p50": round(float(np.median(x)), 2),
+            "max": round(float(x.max()), 2), "min": round(float(x.min()), 2)}
 
 
 def main():
@@ -36,31 +43,41 @@ def main():
     rec = buf[:n]
     cta = (rec[:, 0] >> 32).astype(np.int64)
     role = (rec[:, 0] & 0xFFFFFFFF).astype(np.int64)
+    uid = rec[:, 1].astype(np.int64)
     t0 = rec[:, 2].astype(np.int64)
     t1 = rec[:, 3].astype(np.int64)
     base = t0.min()
-    out = {"records": int(n), "kernel_span_us": float((t1.max() - base) / 1e3)}
-    for r, name in ROLES.items():
-        m = role == r
-        if not m.any():
-            continue
-        dur = (t1[m] - t0[m]) / 1e3
-        out[name] = {"n": int(m.sum()), "mean_us": float(dur.mean()), "max_us": float(dur.max()),
-                     "p50_us": float(np.median(dur)), "last_end_us": float((t1[m].max() - base) / 1e3),
-                     "first_start_us": float((t0[m].min() - base) / 1e3)}
-    ends = collections.defaultdict(int)
-    m = role == 5
-    out["cta_end_us_sorted_tail"] = sorted(((t1[m] - base) / 1e3).tolist())[-10:]
-    out["cta_start_us_sorted_tail"] = sorted(((t0[m] - base) / 1e3).tolist())[-5:]
-    # slowest reduce/combine tasks
-    m = (role == 3) | (role == 6)
-    idx = np.argsort(-(t1[m] - t0[m]))[:8]
-    out["slowest_tasks"] = [{"cta": int(cta[m][i]), "role": int(role[m][i]), "task": int(rec[m][i, 1]),
-                             "start_us": float((t0[m][i] - base) / 1e3), "dur_us": float((t1[m][i] - t0[m][i]) / 1e3)}
-                            for i in idx]
-    m = role == 2
-    e_end = (t1[m] - base) / 1e3
-    out["epilogue_end_p99_us"] = float(np.percentile(e_end, 99))
+    used = layer.used_experts()
+    nrows = int(((torch.bincount(layer.assigned.flatten().long(), minlength=N) + 15) // 16 * 16).sum().item())
+    # unit classes (queue order: gather rows, phase-0, phase-1)
+    tiles1 = 2 * ((ff + 63) // 64) * 64 // 128
+    ngather = nrows
+    nA = used * tiles1
+    out = {"records": int(n), "kernel_span_us": float((t1.max() - base) / 1e3), "ngather": ngather, "nA": nA}
+    m = role == 4
+    dur = (t1[m] - t0[m]) / 1e3
+    u = uid[m]
+    out["mma_phase0"] = stats(dur[(u >= ngather) & (u < ngather + nA)])
+    out["mma_phase1"] = stats(dur[u >= ngather + nA])
+    out["mma_first_start"] = float((t0[m].min() - base) / 1e3)
+    out["mma_last_end"] = float((t1[m].max() - base) / 1e3)
+    # per-CTA MMA busy time and gaps
+    busy, gaps, first, last = [], [], [], []
+    for c in np.unique(cta[m]):
+        mm = m & (cta == c)
+        s, e = np.sort(t0[mm]), np.sort(t1[mm])
+        busy.append((e - s).sum() / 1e3)
+        first.append((s[0] - base) / 1e3)
+        last.append((e[-1] - base) / 1e3)
+        gaps.append(((s[1:] - e[:-1]).clip(min=0)).sum() / 1e3)
+    out["cta_mma_busy"] = stats(busy)
+    out["cta_mma_gaps"] = stats(gaps)
+    out["cta_mma_first"] = stats(first)
+    out["cta_mma_last"] = stats(last)
+    mw = role == 1
+    out["dep_wait"] = stats((t1[mw] - t0[mw]) / 1e3)
+    me = role == 2
+    out["epilogue"] = stats((t1[me] - t0[me]) / 1e3)
     print(json.dumps(out, indent=1))
 
 
