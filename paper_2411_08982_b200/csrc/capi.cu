@@ -237,8 +237,24 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   const PlanOut o = plan_out(ws, P);
 
   uint16_t* x_perm = at<uint16_t>(ws, P.x_perm);
-  record(ev, 0, s);  // K2 (gather) runs inside K3 as its first work units
+  record(ev, 0, s);
   int st = LYNX_OK;
+  static int fused = -1;
+  if (fused < 0) {
+    const char* e = getenv("LYNX_FUSED_GATHER");
+    fused = e ? atoi(e) : 0;
+  }
+  if (!fused) {  // K2 as its own kernel
+    GatherArgs ga;
+    ga.hidden = hidden;
+    ga.perm_token = o.perm_token;
+    ga.n_rows = o.n_rows;
+    ga.rows_cap = c.rows_cap;
+    ga.d = d;
+    ga.x_perm = x_perm;
+    st = cuda_status(launch_gather(ga, sms, s));
+    if (st) return st;
+  }
 
   FfnParams fp;
   {
@@ -270,6 +286,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.kb2_total = g.kb2_total;
   fp.rows_cap = c.rows_cap;
   fp.max_seg = c.max_seg;
+  fp.fused_gather = fused;
   fp.hidden = hidden;
   fp.perm_token = o.perm_token;
   fp.n_rows = o.n_rows;

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 #endif
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
-  const int ngather = (*p.n_rows + kGatherRows - 1) / kGatherRows;
+  const int ngather = p.fused_gather ? (*p.n_rows + kGatherRows - 1) / kGatherRows : 0;
   const int total = ngather + nseg * (p.tiles1 + p.tiles2 * p.split2);
 
   if (warp == 0) {
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       const uint64_t pol_act = policy_evict_last();
       int stage = 0, slot = 0;
       uint32_t phase = 0, uphase = 0;
-      uint64_t known_ready = 0;  // bit 0: gather done; bit 1+s: H of segment s published
+      uint64_t known_ready = p.fused_gather ? 0ull : 1ull;  // bit 0: gather done; bit 1+s: H of segment s
       while (true) {
         int u = atomicAdd(&p.counters[0], 1);
         if (u >= total) u = -1;

@@ -96,6 +96,8 @@ struct FfnParams {
                     // [1 + max_seg] gather chunks done
   int max_seg;
   // fused gather (K2): hidden rows -> permuted segments, first in the queue
+  // (fused_gather = 0: a separate gather kernel already filled x_perm)
+  int fused_gather;
   const uint16_t* hidden;
   const int32_t* perm_token;
   const int32_t* n_rows;
