@@ -53,7 +53,7 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False, src_d
     csrc, inc = CSRC, INCLUDE
     if src_dir is not None:
         csrc, inc = os.path.join(src_dir, "paper_2411_08982_b200", "csrc"), os.path.join(src_dir, "include")
-        build_dir = os.path.join(BUILD, "ab_" + os.path.basename(out).replace(".so", ""))
+        build_dir = os.path.join(BUILD, "ab_" + os.path.basename(out).replace(".so", "") + ("_t" if trace else ""))
         lib_path = out
     os.makedirs(build_dir, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
@@ -86,6 +86,6 @@ if __name__ == "__main__":
         with tempfile.TemporaryDirectory() as tmp:
             subprocess.run(f"git -C {ROOT} archive {rev} paper_2411_08982_b200/csrc include | tar -x -C {tmp}",
                            shell=True, check=True)
-            print(build(verbose=True, force=True, src_dir=tmp, out=out))
+            print(build(verbose=True, force=True, src_dir=tmp, out=out, trace="--trace" in sys.argv))
     else:
         print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv))

@@ -287,6 +287,14 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.rows_cap = c.rows_cap;
   fp.max_seg = c.max_seg;
   fp.fused_gather = fused;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("LYNX_DEBUG_FLAGS");
+      dbg = e ? atoi(e) : 0;
+    }
+    fp.dbg = dbg;
+  }
   fp.hidden = hidden;
   fp.perm_token = o.perm_token;
   fp.n_rows = o.n_rows;

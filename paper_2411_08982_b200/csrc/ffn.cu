@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         // Readiness is sticky: remember it so each dependency costs one
         // acquire load per CTA (an L2 round trip under a saturated HBM is ~1 us).
         const uint64_t dep_bit = U.phase == 0 ? 1ull : (U.seg < 63 ? 2ull << U.seg : 0ull);
-        bool ready = (known_ready & dep_bit) != 0;
+        bool ready = (known_ready & dep_bit) != 0 && !((p.dbg & 1) && U.phase == 1);
         if (!ready && ld_acquire_gpu(dep) >= need) {
           ready = true;
           fence_proxy_async();  // activations written by generic stores, read by TMA

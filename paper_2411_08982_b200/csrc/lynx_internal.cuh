@@ -98,6 +98,7 @@ struct FfnParams {
   // fused gather (K2): hidden rows -> permuted segments, first in the queue
   // (fused_gather = 0: a separate gather kernel already filled x_perm)
   int fused_gather;
+  int dbg;
   const uint16_t* hidden;
   const int32_t* perm_token;
   const int32_t* n_rows;

@@ -51,7 +51,7 @@ def main():
     nrows = int(((torch.bincount(layer.assigned.flatten().long(), minlength=N) + 15) // 16 * 16).sum().item())
     # unit classes (queue order: gather rows, phase-0, phase-1)
     tiles1 = 2 * ((ff + 63) // 64) * 64 // 128
-    ngather = nrows
+    ngather = nrows if os.environ.get("LYNX_FUSED_GATHER", "0") == "1" else 0
     nA = used * tiles1
     out = {"records": int(n), "kernel_span_us": float((t1.max() - base) / 1e3), "ngather": ngather, "nA": nA}
     m = role == 4
