@@ -152,7 +152,7 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.tok_rows = take(sizeof(int32_t) * T * k);
   p.tok_weight = take(sizeof(float) * T * k);
   // unit ticket + phase-0 tiles published per segment
-  p.n_counters = 2 + c.max_seg;  // + gather chunks done
+  p.n_counters = 1 + c.max_seg;
   p.counters = take(sizeof(int32_t) * p.n_counters);
   p.x_perm = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * d);
   p.h = take(sizeof(uint16_t) * static_cast<size_t>(c.rows_cap) * ff);
@@ -236,25 +236,16 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   const Geometry g = geometry(L, T);
   const PlanOut o = plan_out(ws, P);
 
-  uint16_t* x_perm = at<uint16_t>(ws, P.x_perm);
+  GatherArgs ga;
+  ga.hidden = hidden;
+  ga.perm_token = o.perm_token;
+  ga.n_rows = o.n_rows;
+  ga.rows_cap = c.rows_cap;
+  ga.d = d;
+  ga.x_perm = at<uint16_t>(ws, P.x_perm);
   record(ev, 0, s);
-  int st = LYNX_OK;
-  static int fused = -1;
-  if (fused < 0) {
-    const char* e = getenv("LYNX_FUSED_GATHER");
-    fused = e ? atoi(e) : 0;
-  }
-  if (!fused) {  // K2 as its own kernel
-    GatherArgs ga;
-    ga.hidden = hidden;
-    ga.perm_token = o.perm_token;
-    ga.n_rows = o.n_rows;
-    ga.rows_cap = c.rows_cap;
-    ga.d = d;
-    ga.x_perm = x_perm;
-    st = cuda_status(launch_gather(ga, sms, s));
-    if (st) return st;
-  }
+  int st = cuda_status(launch_gather(ga, sms, s));
+  if (st) return st;
 
   FfnParams fp;
   {
@@ -265,7 +256,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
     const uint32_t bw[3] = {64, 128, 1};
     const uint32_t ba[2] = {64, 16};
     if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw) ||
-        !encode_bf16(&fp.map_x, x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
+        !encode_bf16(&fp.map_x, ga.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
       return LYNX_ERR_CUDA;
   }
   fp.n_seg = o.n_seg;
@@ -285,20 +276,6 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.kb2_per = g.kb2_per;
   fp.kb2_total = g.kb2_total;
   fp.rows_cap = c.rows_cap;
-  fp.max_seg = c.max_seg;
-  fp.fused_gather = fused;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("LYNX_DEBUG_FLAGS");
-      dbg = e ? atoi(e) : 0;
-    }
-    fp.dbg = dbg;
-  }
-  fp.hidden = hidden;
-  fp.perm_token = o.perm_token;
-  fp.n_rows = o.n_rows;
-  fp.x_perm = x_perm;
   record(ev, 1, s);
   st = cuda_status(launch_ffn(fp, g.bn, sms, s));
   if (st) return st;

@@ -50,22 +50,12 @@ constexpr int kUnitRing = 4;
 constexpr int kTileA = 128 * 64 * 2;  // 128 weight rows x 64 bf16 (one 128B-swizzled k block)
 constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
 
-constexpr int kGatherRows = 1;        // rows of the permuted buffer per gather unit
-constexpr int kPhaseGather = 2;
-
 struct Unit {
   int phase, seg, mt, split, kb0, kb1, expert, row0, n, nmma;
 };
 
-// Queue order: [gather units][phase-0 units][phase-1 units].
-__device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int ngather, int u, Unit& U) {
+__device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u, Unit& U) {
   if (u < 0) return false;
-  if (u < ngather) {
-    U.phase = kPhaseGather;
-    U.mt = u;
-    return true;
-  }
-  u -= ngather;
   const int nA = nseg * p.tiles1;
   if (u < nA) {
     U.phase = 0;
@@ -168,8 +158,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 #endif
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
-  const int ngather = p.fused_gather ? (*p.n_rows + kGatherRows - 1) / kGatherRows : 0;
-  const int total = ngather + nseg * (p.tiles1 + p.tiles2 * p.split2);
+  const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -178,7 +167,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       const uint64_t pol_act = policy_evict_last();
       int stage = 0, slot = 0;
       uint32_t phase = 0, uphase = 0;
-      uint64_t known_ready = p.fused_gather ? 0ull : 1ull;  // bit 0: gather done; bit 1+s: H of segment s
       while (true) {
         int u = atomicAdd(&p.counters[0], 1);
         if (u >= total) u = -1;
@@ -190,76 +178,32 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           uphase ^= 1;
         }
         Unit U;
-        if (!decode_unit(p, nseg, ngather, u, U)) break;
-        if (U.phase == kPhaseGather) continue;  // done by the epilogue warps
+        if (!decode_unit(p, nseg, u, U)) break;
         const CUtensorMap* ma = U.phase == 0 ? &p.map_w1 : &p.map_w2;
         const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
+        if (U.phase == 1) {
+          LYNX_TRACE_T0;
+          const int* done = p.counters + 1 + U.seg;
+          Watchdog wd;
+          while (ld_acquire_gpu(done) < 4 * p.tiles1) {
+            __nanosleep(100);
+            wd.tick(2);
+          }
+          fence_proxy_async();  // H was written by generic stores; TMA reads it
+          LYNX_TRACE_REC(1, u);
+        }
         const int nb = U.nmma >> 4;
         const uint32_t bytes = kTileA + nb * kBoxB;
-        // The activation tiles depend on earlier units (gathered rows for
-        // phase 0, H for phase 1); the weight tiles never do.  While the
-        // dependency is unmet, keep streaming weight tiles into free stages
-        // and defer their activation loads; issue the deferred ones as soon
-        // as it is met.  (Once met, stages get both loads together.)
-        const int* dep = U.phase == 0 ? p.counters + 1 + p.max_seg : p.counters + 1 + U.seg;
-        const int need = 4 * (U.phase == 0 ? ngather : p.tiles1);  // one release per epilogue warp
-        // Readiness is sticky: remember it so each dependency costs one
-        // acquire load per CTA (an L2 round trip under a saturated HBM is ~1 us).
-        const uint64_t dep_bit = U.phase == 0 ? 1ull : (U.seg < 63 ? 2ull << U.seg : 0ull);
-        bool ready = (known_ready & dep_bit) != 0 && !((p.dbg & 1) && U.phase == 1);
-        if (!ready && ld_acquire_gpu(dep) >= need) {
-          ready = true;
-          fence_proxy_async();  // activations written by generic stores, read by TMA
-        }
-        if (ready) known_ready |= dep_bit;
-        int pend_first = -1, pend_stage = 0;  // deferred k blocks: [pend_first, kb)
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
           mbar_expect_tx(&full[stage], bytes);
           tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
-          if (!ready) {
-            if (pend_first < 0) {
-              pend_first = kb;
-              pend_stage = stage;
-            }
-            ready = ld_acquire_gpu(dep) >= need;
-            if (!ready && kb - pend_first + 1 == STAGES) {  // every stage waits on it: block
-              LYNX_TRACE_T0;
-              Watchdog wd;
-              while (ld_acquire_gpu(dep) < need) {
-                __nanosleep(64);
-                wd.tick(2);
-              }
-              ready = true;
-              LYNX_TRACE_REC(1, u);
-            }
-            if (ready) {
-              known_ready |= dep_bit;
-              fence_proxy_async();
-              for (int k2 = pend_first, st = pend_stage; k2 <= kb; ++k2, st = st + 1 == STAGES ? 0 : st + 1)
-                for (int j = 0; j < nb; ++j)
-                  tma_load_2d(sB + st * kTileB + j * kBoxB, mb, &full[st], k2 * 64, U.row0 + 16 * j, pol_act);
-            }
-          } else {
-            for (int j = 0; j < nb; ++j)
-              tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
-          }
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
-        }
-        if (!ready) {  // unit shorter than the ring and still waiting
-          Watchdog wd;
-          while (ld_acquire_gpu(dep) < need) {
-            __nanosleep(64);
-            wd.tick(2);
-          }
-          known_ready |= dep_bit;
-          fence_proxy_async();
-          for (int k2 = pend_first, st = pend_stage; k2 < U.kb1; ++k2, st = st + 1 == STAGES ? 0 : st + 1)
-            for (int j = 0; j < nb; ++j)
-              tma_load_2d(sB + st * kTileB + j * kBoxB, mb, &full[st], k2 * 64, U.row0 + 16 * j, pol_act);
         }
       }
     }
@@ -277,8 +221,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           uphase ^= 1;
         }
         Unit U;
-        if (!decode_unit(p, nseg, ngather, u, U)) break;
-        if (U.phase == kPhaseGather) continue;
+        if (!decode_unit(p, nseg, u, U)) break;
         const uint32_t idesc = idesc_bf16_f32(128, U.nmma);
         mbar_wait(&tempty[acc], aphase ^ 1, 5);
         LYNX_TRACE_T0;
@@ -319,33 +262,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         uphase ^= 1;
       }
       Unit U;
-      if (!decode_unit(p, nseg, ngather, u, U)) break;
-      if (U.phase == kPhaseGather) {
-        // K2 fused: copy one row of hidden into the permuted buffer (padding
-        // rows zero) with all 4 epilogue warps; the loads of the row are
-        // independent (one memory round trip after the token lookup).
-        const int row = U.mt;
-        const int nvec = p.d >> 3;
-        const int t = p.perm_token[row];
-        const uint4* src = reinterpret_cast<const uint4*>(p.hidden) + static_cast<size_t>(t < 0 ? 0 : t) * nvec;
-        uint4* dst = reinterpret_cast<uint4*>(p.x_perm) + static_cast<size_t>(row) * nvec;
-        for (int i0 = q * 32 + lane; i0 < nvec; i0 += 128 * 4) {
-          uint4 v[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int i = i0 + j * 128;
-            v[j] = (i < nvec && t >= 0) ? src[i] : make_uint4(0, 0, 0, 0);
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (i0 + j * 128 < nvec) dst[i0 + j * 128] = v[j];
-        }
-        __threadfence();
-        fence_proxy_async();  // read back through TMA by phase-0 units
-        __syncwarp();
-        if (lane == 0) red_release_gpu_add(p.counters + 1 + p.max_seg, 1);
-        continue;
-      }
+      if (!decode_unit(p, nseg, u, U)) break;
       mbar_wait(&tfull[acc], aphase, 8);
       LYNX_TRACE_T0;
       tc_fence_after();

@@ -92,17 +92,7 @@ struct FfnParams {
   const int32_t* seg_count;
   uint16_t* h;      // [rows_cap, ff] bf16
   float* partial;   // [split2, rows_cap, d] f32
-  int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s,
-                    // [1 + max_seg] gather chunks done
-  int max_seg;
-  // fused gather (K2): hidden rows -> permuted segments, first in the queue
-  // (fused_gather = 0: a separate gather kernel already filled x_perm)
-  int fused_gather;
-  int dbg;
-  const uint16_t* hidden;
-  const int32_t* perm_token;
-  const int32_t* n_rows;
-  uint16_t* x_perm;
+  int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s
   int d, ff, act;
   int tiles1, kb1;  // phase 0: 128-row tiles per segment, 64-wide k blocks
   int tiles2, split2, kb2_per, kb2_total;
