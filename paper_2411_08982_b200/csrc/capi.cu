@@ -255,8 +255,22 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
     const uint64_t dh[2] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(c.rows_cap)};
     const uint32_t bw[3] = {64, 128, 1};
     const uint32_t ba[2] = {64, 16};
-    if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw) ||
-        !encode_bf16(&fp.map_x, ga.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
+    static int tiled_exp = -1;
+    if (tiled_exp < 0) {
+      const char* e = getenv("LYNX_TILED_EXPERIMENT");
+      tiled_exp = e ? atoi(e) : 0;
+    }
+    fp.tiled = tiled_exp;
+    if (fp.tiled) {  // timing experiment: tile-contiguous addressing of the same buffers
+      const uint64_t t1[2] = {64, static_cast<uint64_t>(N) * g.rows1 * d / 64};
+      const uint64_t t2[2] = {64, static_cast<uint64_t>(N) * d * ff / 64};
+      const uint32_t bt[2] = {64, 128};
+      if (!encode_bf16(&fp.map_w1, L->w13, 2, t1, bt) || !encode_bf16(&fp.map_w2, L->w2, 2, t2, bt))
+        return LYNX_ERR_CUDA;
+    } else if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw)) {
+      return LYNX_ERR_CUDA;
+    }
+    if (!encode_bf16(&fp.map_x, ga.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
       return LYNX_ERR_CUDA;
   }
   fp.n_seg = o.n_seg;

@@ -54,13 +54,7 @@ struct Unit {
   int phase, seg, mt, split, kb0, kb1, expert, row0, n, nmma;
 };
 
-constexpr int kSegCache = 128;  // segment table cached in shared memory (max_seg <= 97)
-
-struct SegCache {
-  int expert[kSegCache], row[kSegCache], count[kSegCache];
-};
-
-__device__ __forceinline__ bool decode_unit(const FfnParams& p, const SegCache* sc, int nseg, int u, Unit& U) {
+__device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u, Unit& U) {
   if (u < 0) return false;
   const int nA = nseg * p.tiles1;
   if (u < nA) {
@@ -81,15 +75,9 @@ __device__ __forceinline__ bool decode_unit(const FfnParams& p, const SegCache* 
     U.kb0 = U.split * p.kb2_per;
     U.kb1 = min(p.kb2_total, U.kb0 + p.kb2_per);
   }
-  if (U.seg < kSegCache) {
-    U.expert = sc->expert[U.seg];
-    U.row0 = sc->row[U.seg];
-    U.n = sc->count[U.seg];
-  } else {
-    U.expert = p.seg_expert[U.seg];
-    U.row0 = p.seg_row[U.seg];
-    U.n = p.seg_count[U.seg];
-  }
+  U.expert = p.seg_expert[U.seg];
+  U.row0 = p.seg_row[U.seg];
+  U.n = p.seg_count[U.seg];
   U.nmma = (U.n + 15) & ~15;
   return true;
 }
@@ -135,7 +123,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   uint64_t* uempty = ufull + kUnitRing;
   int* uring = reinterpret_cast<int*>(uempty + kUnitRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
-  SegCache* sc = reinterpret_cast<SegCache*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -169,16 +156,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 #ifdef LYNX_TRACE
   const uint64_t cta_t0 = globaltimer();
 #endif
-  const int nseg = *p.n_seg;
-  // Segment table -> shared memory once, so unit decoding never waits on a
-  // global load (~1 us under a saturated HBM) at a unit boundary.
-  for (int s = threadIdx.x; s < nseg && s < kSegCache; s += blockDim.x) {
-    sc->expert[s] = p.seg_expert[s];
-    sc->row[s] = p.seg_row[s];
-    sc->count[s] = p.seg_count[s];
-  }
-  __syncthreads();
   const uint32_t tmem_base = *tmem_slot;
+  const int nseg = *p.n_seg;
   const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
 
   if (warp == 0) {
@@ -188,12 +167,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       const uint64_t pol_act = policy_evict_last();
       int stage = 0, slot = 0;
       uint32_t phase = 0, uphase = 0;
-      // The next ticket is taken a few k blocks before the current unit ends,
-      // hiding the atomic's round trip behind streaming.
-      int next_u = atomicAdd(&p.counters[0], 1);
       while (true) {
-        int u = next_u;
-        next_u = -2;
+        int u = atomicAdd(&p.counters[0], 1);
         if (u >= total) u = -1;
         mbar_wait(&uempty[slot], uphase ^ 1, 1);
         uring[slot] = u;
@@ -203,7 +178,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           uphase ^= 1;
         }
         Unit U;
-        if (!decode_unit(p, sc, nseg, u, U)) break;
+        if (!decode_unit(p, nseg, u, U)) break;
         const CUtensorMap* ma = U.phase == 0 ? &p.map_w1 : &p.map_w2;
         const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
         if (U.phase == 1) {
@@ -219,12 +194,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         }
         const int nb = U.nmma >> 4;
         const uint32_t bytes = kTileA + nb * kBoxB;
-        const int kb_ticket = max(U.kb0, U.kb1 - 4);
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
-          if (kb == kb_ticket) next_u = atomicAdd(&p.counters[0], 1);
           mbar_wait(&empty[stage], phase ^ 1, 3);
           mbar_expect_tx(&full[stage], bytes);
-          tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
+          if (p.tiled) {
+            const int tiles = U.phase == 0 ? p.tiles1 : p.tiles2;
+            const int kbs = U.phase == 0 ? p.kb1 : p.kb2_total;
+            tma_load_2d(sA + stage * kTileA, ma, &full[stage], 0, ((U.expert * tiles + U.mt) * kbs + kb) * 128, pol_w);
+          } else {
+            tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
+          }
           for (int j = 0; j < nb; ++j)
             tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
           if (++stage == STAGES) {
@@ -248,7 +227,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
           uphase ^= 1;
         }
         Unit U;
-        if (!decode_unit(p, sc, nseg, u, U)) break;
+        if (!decode_unit(p, nseg, u, U)) break;
         const uint32_t idesc = idesc_bf16_f32(128, U.nmma);
         mbar_wait(&tempty[acc], aphase ^ 1, 5);
         LYNX_TRACE_T0;
@@ -289,7 +268,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         uphase ^= 1;
       }
       Unit U;
-      if (!decode_unit(p, sc, nseg, u, U)) break;
+      if (!decode_unit(p, nseg, u, U)) break;
       mbar_wait(&tfull[acc], aphase, 8);
       LYNX_TRACE_T0;
       tc_fence_after();
@@ -373,8 +352,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 template <int BN, int STAGES>
 static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s) {
   constexpr size_t smem =
-      1024 + STAGES * (kTileA + BN * 128) + (2 * STAGES + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16 +
-      sizeof(SegCache);
+      1024 + STAGES * (kTileA + BN * 128) + (2 * STAGES + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static int configured_device = -1;
   int dev = 0;

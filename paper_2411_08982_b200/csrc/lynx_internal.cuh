@@ -97,6 +97,7 @@ struct FfnParams {
   int tiles1, kb1;  // phase 0: 128-row tiles per segment, 64-wide k blocks
   int tiles2, split2, kb2_per, kb2_total;
   int rows_cap;
+  int tiled;  // weights in tile-contiguous layout (each 128x64 TMA box is one 16 KB run)
 };
 
 // K4: split-K sum + weighted combine (+ residual).
