@@ -41,6 +41,9 @@ CONFIGS = {
                       mode="latency", drop=0, rotate=4),
     "c2-acc": dict(workload="mixtral-8x7b-moe-layer-decode-bs32-lynx-accuracy", d=4096, ff=14336, N=8, k=2,
                    T=32, mode="accuracy", drop=0, rotate=4),
+    # configs[3]: DeepSeek-MoE-16B shape, 64 routed + 2 shared experts, top-6, dynamic (accuracy) selection
+    "c4": dict(workload="deepseek-moe-16b-layer-decode-bs128-lynx-accuracy-budget16", d=2048, ff=1408, N=64, S=2,
+               k=6, T=128, mode="accuracy", drop=0, budget=16, rotate=6),
     # configs[4]: Mixtral-8x22B expert-parallel shape (T is per rank)
     "c5": dict(workload="mixtral-8x22b-moe-layer-decode-lynx-latency-drop4", d=6144, ff=16384, N=8, k=2, T=32,
                mode="latency", drop=4, rotate=3),
@@ -137,8 +140,8 @@ def cpu_layer_setup(c, seed=0):
     T, d, ff, N, k = c["T"], c["d"], c["ff"], c["N"], c["k"]
     router_w = (rng.standard_normal((d, N), dtype=np.float32) * (2.0 / np.sqrt(d))).astype(np.float32)
     batches = [rng.standard_normal((T, d), dtype=np.float32) for _ in range(2)]
-    pol = O.Policy(mode=c["mode"], drop_count=c["drop"])
-    used = set()
+    pol = O.Policy(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
+    used = set(range(N, N + c.get("S", 0)))
     for h in batches:
         ids, probs, full = O.route(O.router_logits(h, router_w).astype(np.float64), k)
         m = O.apply(ids, probs, full, pol)
@@ -148,7 +151,8 @@ def cpu_layer_setup(c, seed=0):
         w1[e] = rng.standard_normal((ff, d), dtype=np.float32) / np.float32(np.sqrt(d))
         w3[e] = rng.standard_normal((ff, d), dtype=np.float32) / np.float32(np.sqrt(d))
         w2[e] = rng.standard_normal((d, ff), dtype=np.float32) / np.float32(np.sqrt(ff))
-    return dict(router_w=router_w, batches=batches, pol=pol, w1=w1, w3=w3, w2=w2, k=k)
+    return dict(router_w=router_w, batches=batches, pol=pol, w1=w1, w3=w3, w2=w2, k=k,
+                shared=range(N, N + c.get("S", 0)))
 
 
 def cpu_layer_step(st, i):
@@ -158,7 +162,13 @@ def cpu_layer_step(st, i):
     h = st["batches"][i % len(st["batches"])]
     ids, probs, full = O.route(O.router_logits(h, st["router_w"]).astype(np.float64), st["k"])
     m = O.apply(ids, probs, full, st["pol"])
-    return O.forward_swiglu(h, st["w1"], st["w3"], st["w2"], m.assigned, m.weights)
+    return O.forward_swiglu(h, st["w1"], st["w3"], st["w2"], m.assigned, m.weights, shared=st["shared"])
+
+
+def policy_name(c):
+    if c["mode"] == "accuracy":
+        return f"accuracy tau 0.5 sample 8 budget {c.get('budget', 4)}"
+    return f"latency drop {c['drop']}"
 
 
 def cpu_threads():
@@ -196,7 +206,7 @@ def run_reference(args, c):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": c["workload"], "d_model": c["d"], "d_ff": c["ff"], "experts": c["N"],
-                   "top_k": c["k"], "tokens": c["T"], "policy": f"{c['mode']} drop {c['drop']}",
+                   "top_k": c["k"], "tokens": c["T"], "policy": policy_name(c),
                    "parallelism": "host"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
                          "sample": "each step = one full layer step of the oracle port (moetrim's "
@@ -213,9 +223,10 @@ def run_single(args, c):
 
     import paper_2411_08982_b200 as L
     T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
-    spec = L.MoEModelSpec(num_layers=n, num_experts=N, top_k=k, d_model=d, d_ff=ff)
+    spec = L.MoEModelSpec(num_layers=n, num_experts=N, top_k=k, d_model=d, d_ff=ff,
+                          num_shared_experts=c.get("S", 0))
     model = L.build_swiglu_model(spec, seed=0)
-    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"])
+    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
     layers = [L.LynxMoELayer(model, l, T, policy=pol) for l in range(n)]
     g = torch.Generator(device="cuda").manual_seed(1)
     hid = [torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
@@ -265,24 +276,22 @@ def run_single(args, c):
             for j, nm in enumerate(names)}
     step_b = statistics.mean(evs[i][0].elapsed_time(evs[i][5]) for i in range(kp))
 
-    # (C) end to end through the public API with pinned host buffers
+    # (C) end to end through the public API with pinned host buffers: every
+    # step copies its input host->device and its output device->host
+    # (LynxMoELayer.host_step replays H2D + layer + D2H as one CUDA graph)
     h_host = [h.cpu().pin_memory() for h in hid]
     o_host = [torch.empty_like(h_host[0]).pin_memory() for _ in range(n)]
     for i in range(n):
-        hid[i].copy_(h_host[i], non_blocking=True)
-        layers[i](hid[i], outs[i])
-        o_host[i].copy_(outs[i], non_blocking=True)
+        layers[i].host_step(h_host[i], o_host[i])
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record()
     for i in range(args.steps):
-        l = i % n
-        hid[l].copy_(h_host[l], non_blocking=True)
-        layers[l](hid[l], outs[l])
-        o_host[l].copy_(outs[l], non_blocking=True)
+        layers[i % n].host_step(h_host[i % n], o_host[i % n])
     c1.record()
     torch.cuda.synchronize()
     ms_e2e = c0.elapsed_time(c1) / args.steps
+    assert torch.equal(o_host[0], outs[0].cpu()), "host_step output differs from the device-resident call"
 
     # algorithmic bytes of one layer step (used experts only) and of one FFN launch
     mean_used = statistics.mean(used[i % n] for i in range(kp))
@@ -297,10 +306,11 @@ def run_single(args, c):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
         "config": {"workload": c["workload"], "d_model": d, "d_ff": ff, "experts": N, "top_k": k,
-                   "global_batch": T, "tokens_per_gpu": T, "policy": f"{c['mode']} drop {c['drop']}",
+                   "global_batch": T, "tokens_per_gpu": T, "policy": policy_name(c),
                    "parallelism": "single", "weight_copies": n,
+                   "shared_experts": c.get("S", 0),
                    "l2": f"inputs > L2: {n} rotating layer copies "
-                         f"({n * N * SWIGLU_BYTES(c) / 1e9:.1f} GB) >> 126 MB L2",
+                         f"({n * (N + c.get('S', 0)) * SWIGLU_BYTES(c) / 1e9:.1f} GB) >> 126 MB L2",
                    "used_experts_per_copy": used, "mean_used_experts": mean_used},
         "roofline": {"bound": "hbm", "kernel": "ffn_kernel (K3, tcgen05 grouped SwiGLU)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -314,7 +324,7 @@ def run_single(args, c):
         "kernel_ms": kern, "profiled_step_ms": step_b,
         "e2e": {"value": T / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2,
-                "api": "paper_2411_08982_b200.LynxMoELayer.__call__ (lynx_moe_layer C ABI), eager"},
+                "api": "paper_2411_08982_b200.LynxMoELayer.host_step (H2D + lynx_moe_layer + D2H, one CUDA graph)"},
         "gpu_launches": 5 * args.steps,
         "clocks": clocks.summary(),
     }

@@ -64,6 +64,7 @@ enum lynx_status {
 /* Build limits. */
 #define LYNX_MAX_EXPERTS 64
 #define LYNX_MAX_TOPK 8
+#define LYNX_MAX_SHARED 4         /* always-on shared experts per layer (DeepSeek-MoE style) */
 #define LYNX_MAX_TOKENS 4096
 #define LYNX_SEG_ROWS 256        /* max token rows one expert segment feeds one MMA */
 
@@ -107,11 +108,15 @@ typedef struct lynx_layer {
   int32_t d_model;        /* d, multiple of 8 */
   int32_t d_ff;           /* ff, multiple of 8 */
   int32_t activation;     /* lynx_activation */
-  int32_t reserved;
-  /* SWIGLU: packed gate/up [N, 2*ceil64(ff), d] (lynx_pack_w13 layout).
-   * TANH2:  w1^T [N, ff, d] (reference w1 is [N, d, ff], simulator.py:40). */
+  /* S shared experts (0..LYNX_MAX_SHARED): experts N..N+S-1 of w13/w2, applied
+   * to every token with gate weight 1 after the routed experts, outside the
+   * router and the policy.  The reference has none; 0
+   * reproduces forward_layer exactly. */
+  int32_t num_shared;
+  /* SWIGLU: packed gate/up [N+S, 2*ceil64(ff), d] (lynx_pack_w13 layout).
+   * TANH2:  w1^T [N+S, ff, d] (reference w1 is [N, d, ff], simulator.py:40). */
   const uint16_t *w13;
-  const uint16_t *w2;        /* [N, d, ff]  (reference w2 [N, ff, d] transposed) */
+  const uint16_t *w2;        /* [N+S, d, ff]  (reference w2 [N, ff, d] transposed) */
   const uint16_t *router_wt; /* [N, d]      (reference router_w [d, N] transposed); may be NULL
                                 if the caller routes itself */
 } lynx_layer_t;
@@ -182,7 +187,8 @@ int lynx_moe_forward(const lynx_layer_t *layer, const uint16_t *hidden, int T,
                      void *workspace, size_t workspace_bytes, lynx_stream_t stream);
 
 /* Same as lynx_moe_forward but writes the f32 sum of expert outputs WITHOUT
- * the residual; assigned entries < 0 are skipped (expert-parallel partial). */
+ * the residual; assigned entries < 0 are skipped (expert-parallel partial).
+ * Shared experts are not part of an expert-parallel shard (num_shared must be 0). */
 int lynx_moe_forward_partial(const lynx_layer_t *layer, const uint16_t *hidden, int T,
                              const int32_t *assigned, const double *weights, float *partial_out,
                              void *workspace, size_t workspace_bytes, lynx_stream_t stream);

@@ -362,7 +362,7 @@ def silu(x):
 
 
 def forward_swiglu(hidden, w1, w3, w2, assigned, weights, dtype=np.float32,
-                   round_h_bf16: bool = False):
+                   round_h_bf16: bool = False, shared=()):
     """forward_layer (simulator.py:86-113) with a SwiGLU expert.
 
     hidden [T, d]; w1, w3 [E, ff, d]; w2 [E, d, ff] (HF Mixtral / K-major
@@ -370,6 +370,9 @@ def forward_swiglu(hidden, w1, w3, w2, assigned, weights, dtype=np.float32,
     merged-weight combine in ascending expert order, like the reference.
     ``round_h_bf16`` rounds the intermediate activation to bf16 the way
     the CUDA kernel stores it (used to tighten tolerances, not required).
+    ``shared`` lists always-on experts (indices into w1/w3/w2) applied to
+    every token with weight 1 after the routed experts, in the given order
+    -- the builder's DeepSeek-MoE extension; the reference has none.
     """
     x = np.asarray(hidden, dtype=dtype)
     if x.shape[0] != assigned.shape[0]:
@@ -377,15 +380,19 @@ def forward_swiglu(hidden, w1, w3, w2, assigned, weights, dtype=np.float32,
             f"mask covers {assigned.shape[0]} tokens but hidden has {x.shape[0]}")
     out = x.copy()
     disp = dispatch(assigned, weights)
-    for e, rows, rw in zip(disp.experts, disp.rows, disp.row_weight):
-        xr = x[rows]
+
+    def expert(e, xr):
         g = xr @ np.asarray(w1[e], dtype=dtype).T
         u = xr @ np.asarray(w3[e], dtype=dtype).T
         h = (silu(g) * u).astype(dtype)
         if round_h_bf16:
             h = bf16_round(h)
-        y = h @ np.asarray(w2[e], dtype=dtype).T
-        out[rows] += rw.astype(dtype)[:, None] * y
+        return h @ np.asarray(w2[e], dtype=dtype).T
+
+    for e, rows, rw in zip(disp.experts, disp.rows, disp.row_weight):
+        out[rows] += rw.astype(dtype)[:, None] * expert(e, x[rows])
+    for e in shared:
+        out += expert(e, x)
     return out
 
 

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get(
 
 # include/lynx_b200.h constants
 LYNX_OK = 0
-ABI_VERSION = 2
+ABI_VERSION = 3
 STATUS = {
     -1: "invalid shape", -2: "k out of range", -3: "min_experts must be >= top_k",
     -4: "retained set empty or out of range", -5: "token count mismatch", -6: "CUDA error",
@@ -26,7 +26,7 @@ STATUS = {
 }
 VALIDATION_CODES = {-1, -2, -3, -4, -5, -7, -9}
 FLAG_CLIPPED, FLAG_NONFINITE, FLAG_ZERO_MASS = 1, 2, 4
-MAX_EXPERTS, MAX_TOPK, MAX_TOKENS, SEG_ROWS = 64, 8, 4096, 256
+MAX_EXPERTS, MAX_TOPK, MAX_TOKENS, SEG_ROWS, MAX_SHARED = 64, 8, 4096, 256, 4
 POLICY_NONE, POLICY_LATENCY, POLICY_ACCURACY = 0, 1, 2
 CONF_TOP1, CONF_MARGIN = 0, 1
 ACT_SWIGLU, ACT_TANH2 = 0, 1
@@ -52,7 +52,7 @@ class LynxSelection(ctypes.Structure):
 class LynxLayer(ctypes.Structure):
     _fields_ = [("num_experts", ctypes.c_int32), ("top_k", ctypes.c_int32),
                 ("d_model", ctypes.c_int32), ("d_ff", ctypes.c_int32),
-                ("activation", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("activation", ctypes.c_int32), ("num_shared", ctypes.c_int32),
                 ("w13", _p), ("w2", _p), ("router_wt", _p)]
 
 

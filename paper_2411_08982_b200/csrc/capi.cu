@@ -20,7 +20,7 @@ using namespace lynx;
 
 namespace {
 
-constexpr int kAbiVersion = 2;
+constexpr int kAbiVersion = 3;
 
 int sm_count_cached() {
   static int cached_dev = -1, cached = 0;
@@ -82,11 +82,15 @@ struct Caps {
   int max_seg, rows_cap;
 };
 
-Caps caps_for(int T, int N, int k) {
+// S shared experts add S segments-per-256-tokens and S 16-padded copies of
+// the T token rows after the routed experts.
+Caps caps_for(int T, int N, int k, int S = 0) {
   const int slots = T * k;
+  const int seg_per_shared = (T + LYNX_SEG_ROWS - 1) / LYNX_SEG_ROWS;
   Caps c;
-  c.max_seg = std::min(N, slots) + slots / LYNX_SEG_ROWS + 1;
-  c.rows_cap = static_cast<int>(align_up(static_cast<size_t>(slots) + 15 * std::min(N, slots), 16));
+  c.max_seg = std::min(N, slots) + slots / LYNX_SEG_ROWS + 1 + S * seg_per_shared;
+  c.rows_cap = static_cast<int>(align_up(static_cast<size_t>(slots) + 15 * std::min(N, slots), 16) +
+                                static_cast<size_t>(S) * align_up(T, 16));
   return c;
 }
 
@@ -118,8 +122,8 @@ struct Plan {
 };
 
 Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
-  const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
-  const Caps c = caps_for(T, N, k);
+  const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff, S = L->num_shared;
+  const Caps c = caps_for(T, N, k, S);
   const Geometry g = geometry(L, T);
   Plan p{};
   size_t off = 0;
@@ -149,8 +153,8 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.seg_count = take(sizeof(int32_t) * c.max_seg);
   p.perm_token = take(sizeof(int32_t) * c.rows_cap);
   p.perm_weight = take(sizeof(float) * c.rows_cap);
-  p.tok_rows = take(sizeof(int32_t) * T * k);
-  p.tok_weight = take(sizeof(float) * T * k);
+  p.tok_rows = take(sizeof(int32_t) * T * (k + S));
+  p.tok_weight = take(sizeof(float) * T * (k + S));
   // unit ticket + phase-0 tiles published per segment
   p.n_counters = 1 + c.max_seg;
   p.counters = take(sizeof(int32_t) * p.n_counters);
@@ -177,6 +181,8 @@ int check_layer(const lynx_layer_t* L, int T, bool slots_exceed_ok = false) {
     return LYNX_ERR_UNSUPPORTED;
   if (L->d_model % 8 || L->d_ff % 8) return LYNX_ERR_UNSUPPORTED;  // TMA 16-byte strides
   if (L->activation != LYNX_ACT_SWIGLU && L->activation != LYNX_ACT_TANH2) return LYNX_ERR_CONFIG;
+  if (L->num_shared < 0) return LYNX_ERR_SHAPE;
+  if (L->num_shared > LYNX_MAX_SHARED) return LYNX_ERR_UNSUPPORTED;
   if (!L->w13 || !L->w2) return LYNX_ERR_SHAPE;
   return LYNX_OK;
 }
@@ -203,9 +209,10 @@ int check_policy(const lynx_policy_t* pol, int k, int decode, int* floor_keep) {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? LYNX_OK : LYNX_ERR_CUDA; }
 
-PlanOut plan_out(void* ws, const Plan& P) {
+PlanOut plan_out(void* ws, const Plan& P, int n_shared) {
   PlanOut o;
   o.enabled = 1;
+  o.n_shared = n_shared;
   o.n_seg = at<int32_t>(ws, P.n_seg);
   o.n_used = at<int32_t>(ws, P.n_used);
   o.n_rows = at<int32_t>(ws, P.n_rows);
@@ -229,12 +236,12 @@ inline void record(cudaEvent_t const* ev, int i, cudaStream_t s) {
 // ev (optional): [0] before K2 (gather), [1] before K3 (FFN), [2] before K4 (combine).
 int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_t* out_bf16, float* out_f32,
                    void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev) {
-  const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff;
+  const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff, S = L->num_shared;
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
-  const Caps c = caps_for(T, N, k);
+  const Caps c = caps_for(T, N, k, S);
   const Geometry g = geometry(L, T);
-  const PlanOut o = plan_out(ws, P);
+  const PlanOut o = plan_out(ws, P, S);
 
   GatherArgs ga;
   ga.hidden = hidden;
@@ -249,27 +256,14 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
 
   FfnParams fp;
   {
-    const uint64_t dw1[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(g.rows1), static_cast<uint64_t>(N)};
-    const uint64_t dw2[3] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(d), static_cast<uint64_t>(N)};
+    const uint64_t dw1[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(g.rows1), static_cast<uint64_t>(N + S)};
+    const uint64_t dw2[3] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(d), static_cast<uint64_t>(N + S)};
     const uint64_t dx[2] = {static_cast<uint64_t>(d), static_cast<uint64_t>(c.rows_cap)};
     const uint64_t dh[2] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(c.rows_cap)};
     const uint32_t bw[3] = {64, 128, 1};
     const uint32_t ba[2] = {64, 16};
-    static int tiled_exp = -1;
-    if (tiled_exp < 0) {
-      const char* e = getenv("LYNX_TILED_EXPERIMENT");
-      tiled_exp = e ? atoi(e) : 0;
-    }
-    fp.tiled = tiled_exp;
-    if (fp.tiled) {  // timing experiment: tile-contiguous addressing of the same buffers
-      const uint64_t t1[2] = {64, static_cast<uint64_t>(N) * g.rows1 * d / 64};
-      const uint64_t t2[2] = {64, static_cast<uint64_t>(N) * d * ff / 64};
-      const uint32_t bt[2] = {64, 128};
-      if (!encode_bf16(&fp.map_w1, L->w13, 2, t1, bt) || !encode_bf16(&fp.map_w2, L->w2, 2, t2, bt))
-        return LYNX_ERR_CUDA;
-    } else if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw)) {
+    if (!encode_bf16(&fp.map_w1, L->w13, 3, dw1, bw) || !encode_bf16(&fp.map_w2, L->w2, 3, dw2, bw))
       return LYNX_ERR_CUDA;
-    }
     if (!encode_bf16(&fp.map_x, ga.x_perm, 2, dx, ba) || !encode_bf16(&fp.map_h, at<uint16_t>(ws, P.h), 2, dh, ba))
       return LYNX_ERR_CUDA;
   }
@@ -300,7 +294,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   ca.slot_stride = static_cast<size_t>(c.rows_cap) * d;
   ca.split2 = g.split2;
   ca.T = T;
-  ca.k = k;
+  ca.k = k + S;
   ca.d = d;
   ca.tok_rows = o.tok_rows;
   ca.tok_weight = o.tok_weight;
@@ -338,10 +332,12 @@ int moe_forward_common(const lynx_layer_t* layer, const uint16_t* hidden, int T,
                        size_t workspace_bytes, cudaStream_t stream) {
   int st = check_layer(layer, T, out_f32 != nullptr);
   if (st) return st;
+  if (out_f32 && layer->num_shared) return LYNX_ERR_UNSUPPORTED;
   const Plan P = plan_for(layer, T, false);
   if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
   void* ws = aligned_ws(workspace);
-  st = cuda_status(launch_plan(assigned, weights, T, layer->num_experts, layer->top_k, plan_out(ws, P), stream));
+  st = cuda_status(launch_plan(assigned, weights, T, layer->num_experts, layer->top_k,
+                               plan_out(ws, P, layer->num_shared), stream));
   if (st) return st;
   return gather_and_ffn(layer, hidden, T, out_bf16, out_f32, ws, P, stream, nullptr);
 }
@@ -379,7 +375,7 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   a.important = LYNX_PICK(important, important, uint8_t);
   a.flags = LYNX_PICK(flags, flags, int32_t);
 #undef LYNX_PICK
-  a.plan = plan_out(ws, P);
+  a.plan = plan_out(ws, P, layer->num_shared);
   record(ev, 1, stream);
   st = cuda_status(launch_route_select(a, stream));
   if (st) return st;
@@ -527,6 +523,7 @@ int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t*
   const Caps c = caps_for(T, N, k);
   PlanOut o;
   o.enabled = 1;
+  o.n_shared = 0;
   o.n_seg = out->n_seg;
   o.n_used = out->n_used;
   o.n_rows = out->n_rows;

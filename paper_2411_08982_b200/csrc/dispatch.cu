@@ -46,8 +46,8 @@ cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
 // the layer output is bit-reproducible.  One CTA per (token, 512 columns);
 // the token's rows are staged once, then all k*S float4 loads issue together.
 __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
-  __shared__ int s_rows[LYNX_MAX_TOPK];
-  __shared__ float s_w[LYNX_MAX_TOPK];
+  __shared__ int s_rows[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
+  __shared__ float s_w[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
   griddep_launch_dependents();
   griddep_wait();  // partial slots come from K3
   const int t = blockIdx.y;

@@ -197,13 +197,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
           mbar_expect_tx(&full[stage], bytes);
-          if (p.tiled) {
-            const int tiles = U.phase == 0 ? p.tiles1 : p.tiles2;
-            const int kbs = U.phase == 0 ? p.kb1 : p.kb2_total;
-            tma_load_2d(sA + stage * kTileA, ma, &full[stage], 0, ((U.expert * tiles + U.mt) * kbs + kb) * 128, pol_w);
-          } else {
-            tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
-          }
+          tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
           for (int j = 0; j < nb; ++j)
             tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
           if (++stage == STAGES) {

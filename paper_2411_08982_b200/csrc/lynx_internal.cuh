@@ -46,6 +46,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 // Dispatch plan written by K1 (or the standalone plan kernel).
 struct PlanOut {
   int enabled;
+  int n_shared;         // S always-on experts N..N+S-1 over all T tokens (tok_rows stride k+S)
   int32_t* n_seg;
   int32_t* n_used;
   int32_t* n_rows;      // rows of the permuted buffer in use (16-padded per expert)
@@ -54,8 +55,8 @@ struct PlanOut {
   int32_t* seg_count;
   int32_t* perm_token;  // [rows_cap] source token, -1 = padding
   float* perm_weight;
-  int32_t* tok_rows;    // [T,k] permuted rows per token, experts ascending, -1 padded
-  float* tok_weight;
+  int32_t* tok_rows;    // [T,k+S] permuted rows per token: routed experts ascending (-1 padded),
+  float* tok_weight;    //   then the S shared experts (weight 1)
   int* counters;        // FFN scheduler words zeroed for the next K3 launch
   int n_counters;
 };
@@ -97,7 +98,6 @@ struct FfnParams {
   int tiles1, kb1;  // phase 0: 128-row tiles per segment, 64-wide k blocks
   int tiles2, split2, kb2_per, kb2_total;
   int rows_cap;
-  int tiled;  // weights in tile-contiguous layout (each 128x64 TMA box is one 16 KB run)
 };
 
 // K4: split-K sum + weighted combine (+ residual).
@@ -105,7 +105,7 @@ struct CombineArgs {
   const uint16_t* hidden;  // residual; null -> no residual (EP partial)
   const float* partial;    // [split2][rows_cap][d]
   size_t slot_stride;      // rows_cap * d
-  int split2, T, k, d;
+  int split2, T, k, d;  // k = entries per token in tok_rows (top_k + shared)
   const int32_t* tok_rows;
   const float* tok_weight;
   uint16_t* out_bf16;  // exactly one of the outputs is set

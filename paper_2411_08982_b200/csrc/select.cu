@@ -24,6 +24,7 @@
 // size is latency.
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lynx_internal.cuh"
 #include "ptx.cuh"
@@ -210,7 +211,9 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
                                            const PlanOut& o, uint32_t* s_bits, int* s_prefix) {
   __shared__ int s_cnt[LYNX_MAX_EXPERTS];
   __shared__ int s_base[LYNX_MAX_EXPERTS];
+  __shared__ int s_shared_base;
   const int W = (T + 31) >> 5;
+  const int S = o.n_shared, kk = k + S, T16 = (T + 15) & ~15;
   const int tid = threadIdx.x, nthr = blockDim.x;
   #pragma unroll 1
   for (int i = tid; i < N * W; i += nthr) s_bits[i] = 0;
@@ -234,71 +237,111 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     }
     s_cnt[e] = run;
   }
-  __syncthreads();
-  if (tid == 0) {
-    int base = 0, nseg = 0, nused = 0;
-    #pragma unroll 1
-    for (int e = 0; e < N; ++e) {
-      const int cnt = s_cnt[e];
-      s_base[e] = base;
-      if (cnt == 0) continue;
-      ++nused;
-      #pragma unroll 1
-      for (int c0 = 0; c0 < cnt; c0 += LYNX_SEG_ROWS) {
-        o.seg_expert[nseg] = e;
-        o.seg_row[nseg] = base + c0;
-        o.seg_count[nseg] = min(LYNX_SEG_ROWS, cnt - c0);
-        ++nseg;
-      }
-      base += (cnt + 15) & ~15;
-    }
-    *o.n_seg = nseg;
-    *o.n_used = nused;
-    *o.n_rows = base;
-  }
   #pragma unroll 1
   for (int i = tid; i < o.n_counters; i += nthr) o.counters[i] = 0;
   __syncthreads();
+  if (tid < 32) {
+    // Expert bases and segment slots: one warp scans the 16-padded row counts
+    // and segment counts over experts ascending (lane l: experts l, l + 32).
+    const int lane = tid;
+    int cnt[2], pad[2], nsg[2], base[2], seg[2];
+    #pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      cnt[h] = e < N ? s_cnt[e] : 0;
+      pad[h] = (cnt[h] + 15) & ~15;
+      nsg[h] = (cnt[h] + LYNX_SEG_ROWS - 1) / LYNX_SEG_ROWS;
+    }
+    int row_off = 0, seg_off = 0;
+    #pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int rs = pad[h], ss = nsg[h];
+      #pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int r2 = __shfl_up_sync(kFull, rs, off), s2 = __shfl_up_sync(kFull, ss, off);
+        if (lane >= off) {
+          rs += r2;
+          ss += s2;
+        }
+      }
+      base[h] = row_off + rs - pad[h];
+      seg[h] = seg_off + ss - nsg[h];
+      row_off += __shfl_sync(kFull, rs, 31);
+      seg_off += __shfl_sync(kFull, ss, 31);
+    }
+    #pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      if (e < N) s_base[e] = base[h];
+      #pragma unroll 1
+      for (int c = 0; c < nsg[h]; ++c) {
+        o.seg_expert[seg[h] + c] = e;
+        o.seg_row[seg[h] + c] = base[h] + c * LYNX_SEG_ROWS;
+        o.seg_count[seg[h] + c] = min(LYNX_SEG_ROWS, cnt[h] - c * LYNX_SEG_ROWS);
+      }
+    }
+    const int nused = __popc(__ballot_sync(kFull, cnt[0] > 0)) + __popc(__ballot_sync(kFull, cnt[1] > 0));
+    // shared experts: every token, in token order, after the routed experts
+    const int seg_per_shared = (T + LYNX_SEG_ROWS - 1) / LYNX_SEG_ROWS;
+    #pragma unroll 1
+    for (int i = lane; i < S * seg_per_shared; i += 32) {
+      const int sx = i / seg_per_shared, c = i - sx * seg_per_shared;
+      o.seg_expert[seg_off + i] = N + sx;
+      o.seg_row[seg_off + i] = row_off + sx * T16 + c * LYNX_SEG_ROWS;
+      o.seg_count[seg_off + i] = min(LYNX_SEG_ROWS, T - c * LYNX_SEG_ROWS);
+    }
+    if (lane == 0) {
+      s_shared_base = row_off;
+      *o.n_seg = seg_off + S * seg_per_shared;
+      *o.n_used = nused + S;
+      *o.n_rows = row_off + S * T16;
+    }
+  }
+  __syncthreads();
+  // Per token: its distinct experts ascending (bit scan of a 64-bit set), the
+  // permuted row of each and the merged weight 0 + sum of its slots on that
+  // expert in slot order (simulator.py:108-111).
   #pragma unroll 1
   for (int t = tid; t < T; t += nthr) {
-    int ids[LYNX_MAX_TOPK];
-    int n = 0;
-    #pragma unroll 1
-    for (int c = 0; c < k; ++c) {
-      const int e = asg[t * k + c];
-      if (e < 0 || e >= N) continue;
-      bool dup = false;
-      #pragma unroll 1
-      for (int j = 0; j < n; ++j) dup |= ids[j] == e;
-      if (dup) continue;
-      int j = n++;
-      while (j > 0 && ids[j - 1] > e) {
-        ids[j] = ids[j - 1];
-        --j;
-      }
-      ids[j] = e;
+    int a_r[LYNX_MAX_TOPK];
+    uint64_t set = 0;
+    #pragma unroll
+    for (int c = 0; c < LYNX_MAX_TOPK; ++c) {
+      a_r[c] = c < k ? asg[t * k + c] : -1;
+      if (a_r[c] >= 0 && a_r[c] < N) set |= 1ull << a_r[c];
     }
-    #pragma unroll 1
-    for (int j = 0; j < n; ++j) {
-      const int e = ids[j];
+    int j = 0;
+    while (set) {
+      const int e = __ffsll(static_cast<long long>(set)) - 1;
+      set &= set - 1;
       const uint32_t word = s_bits[e * W + (t >> 5)];
       const int row = s_base[e] + s_prefix[e * W + (t >> 5)] + __popc(word & ((1u << (t & 31)) - 1u));
       double acc = 0.0;
-      #pragma unroll 1
-      for (int c = 0; c < k; ++c)
-        if (asg[t * k + c] == e) acc += w[t * k + c];
+      #pragma unroll
+      for (int c = 0; c < LYNX_MAX_TOPK; ++c)
+        if (a_r[c] == e) acc += w[t * k + c];
       const float wf = static_cast<float>(acc);
-      o.tok_rows[t * k + j] = row;
-      o.tok_weight[t * k + j] = wf;
+      o.tok_rows[t * kk + j] = row;
+      o.tok_weight[t * kk + j] = wf;
       o.perm_token[row] = t;
       o.perm_weight[row] = wf;
+      ++j;
     }
     #pragma unroll 1
-    for (int j = n; j < k; ++j) {
-      o.tok_rows[t * k + j] = -1;
-      o.tok_weight[t * k + j] = 0.f;
+    for (; j < k; ++j) {
+      o.tok_rows[t * kk + j] = -1;
+      o.tok_weight[t * kk + j] = 0.f;
+    }
+    #pragma unroll 1
+    for (int sx = 0; sx < S; ++sx) {
+      const int row = s_shared_base + sx * T16 + t;
+      o.tok_rows[t * kk + k + sx] = row;
+      o.tok_weight[t * kk + k + sx] = 1.f;
+      o.perm_token[row] = t;
+      o.perm_weight[row] = 1.f;
     }
   }
+  // zero the 16-row padding of every segment run
   #pragma unroll 1
   for (int e = tid; e < N; e += nthr) {
     const int cnt = s_cnt[e];
@@ -307,6 +350,12 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
       o.perm_token[r] = -1;
       o.perm_weight[r] = 0.f;
     }
+  }
+  #pragma unroll 1
+  for (int i = tid; i < S * (T16 - T); i += nthr) {
+    const int row = s_shared_base + (i / (T16 - T)) * T16 + T + i % (T16 - T);
+    o.perm_token[row] = -1;
+    o.perm_weight[row] = 0.f;
   }
 }
 
@@ -469,12 +518,17 @@ __device__ unsigned long long g_sel_ts[16];
     __syncthreads();                                   \
     if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
   } while (0)
+#define SEL_TS_LOCAL(i) \
+  do {                                                 \
+    if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
+  } while (0)
 #else
 #define SEL_TS(i) (void)0
+#define SEL_TS_LOCAL(i) (void)0
 #endif
 
 // ------------------------------------------------------------------- K1
-__global__ void __launch_bounds__(kSelectThreads) route_select_kernel(SelectArgs a) {
+__global__ void __launch_bounds__(kSelectThreads) route_select_kernel(const __grid_constant__ SelectArgs a) {
   __shared__ double s_counts[LYNX_MAX_EXPERTS];
   __shared__ int s_icount[LYNX_MAX_EXPERTS];
   __shared__ int s_rank[LYNX_MAX_EXPERTS];
@@ -645,7 +699,7 @@ __device__ __forceinline__ double reg_at(const double (&p)[NT], int e) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kSelectThreads) route_select_fast(SelectArgs a) {
+__global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid_constant__ SelectArgs a) {
   __shared__ double s_counts[LYNX_MAX_EXPERTS];
   __shared__ int s_icount[LYNX_MAX_EXPERTS];
   __shared__ int s_rank[LYNX_MAX_EXPERTS];
@@ -811,9 +865,304 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(SelectArgs a
   SEL_TS(6);
 }
 
+// --------------------------------------- K1 group path (16 < N <= 64)
+// Eight lanes per token, four tokens per warp, 128 tokens per pass of the
+// CTA.  Lane j of a group holds experts j, j+8, j+16, ... (EPL of them), so
+// numpy's pairwise row sum maps exactly onto the group: lane j runs numpy's
+// j-th strided partial in register, and three xor-shuffles fold
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) -- IEEE addition is commutative, so
+// every lane's fold is the same bits as numpy's.  Arg-max rounds (top-k,
+// remap picks) are an in-lane scan plus three shuffles.
+constexpr int kGroup = 8;
+
+// value of element e (lane e%8, slot e/8) of a group row, on every lane
+template <int EPL>
+__device__ __forceinline__ double grp_at(const double (&v)[EPL], int e, int gbase) {
+  double mine = 0.0;
+#pragma unroll
+  for (int m = 0; m < EPL; ++m)
+    if (m == (e >> 3)) mine = v[m];
+  return __shfl_sync(kFull, mine, gbase + (e & 7));
+}
+
+// numpy pairwise sum of the first n (<= 128) elements of a group row
+template <int EPL>
+__device__ __forceinline__ double grp_pairwise(const double (&v)[EPL], int n, int j, int gbase) {
+  if (n < 8) {
+    double acc = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) acc += __shfl_sync(kFull, v[0], gbase + i);
+    return acc;
+  }
+  const int body = n - (n & 7);
+  double r = v[0];
+#pragma unroll
+  for (int m = 1; m < EPL; ++m)
+    if (8 * m < body) r += v[m];
+  r += __shfl_xor_sync(kFull, r, 1);
+  r += __shfl_xor_sync(kFull, r, 2);
+  r += __shfl_xor_sync(kFull, r, 4);
+#pragma unroll 1
+  for (int i = body; i < n; ++i) r += grp_at<EPL>(v, i, gbase);
+  (void)j;
+  return r;
+}
+
+// best expert of `cand` by (value desc, index asc) over a group row; -1 if
+// none.  (Comparing the doubles' bit patterns as 64-bit integers instead was
+// measured 30% slower: 64-bit integer compares are multi-instruction.)
+template <int EPL>
+__device__ __forceinline__ int grp_best(const double (&v)[EPL], uint64_t cand, int j, double* bv) {
+  int bi = -1;
+  double best = 0.0;
+#pragma unroll
+  for (int m = 0; m < EPL; ++m) {
+    const int e = j + 8 * m;
+    if (((cand >> e) & 1ull) && (bi < 0 || v[m] > best)) {  // ascending e: ties keep the smaller
+      bi = e;
+      best = v[m];
+    }
+  }
+#pragma unroll
+  for (int off = 1; off < kGroup; off <<= 1) {
+    const double ov = __shfl_xor_sync(kFull, best, off);
+    const int oi = __shfl_xor_sync(kFull, bi, off);
+    if (oi >= 0 && (bi < 0 || ov > best || (ov == best && oi < bi))) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  *bv = best;
+  return bi;
+}
+
+template <int EPL>
+__global__ void __launch_bounds__(kSelectThreads) route_select_group(const __grid_constant__ SelectArgs a) {
+  __shared__ double s_counts[LYNX_MAX_EXPERTS];
+  __shared__ int s_icount[LYNX_MAX_EXPERTS];
+  __shared__ int s_rank[LYNX_MAX_EXPERTS];
+  __shared__ int s_order[LYNX_MAX_EXPERTS];
+  __shared__ int s_keep[LYNX_MAX_EXPERTS];
+  __shared__ int s_flags, s_nq, s_clipped;
+  __shared__ unsigned long long s_keepmask;
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+
+  griddep_launch_dependents();
+  const int T = a.T, N = a.N, k = a.k;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int j = tid & 7, gbase = tid & 24, grp = tid >> 3, ngrp = nthr >> 3;
+  const SelectSmem L = select_smem(T, N, k, a.stage, a.plan.enabled);
+  double* P = a.stage ? reinterpret_cast<double*>(s_dyn + L.p) : a.full;
+  double* CONF = a.stage ? reinterpret_cast<double*>(s_dyn + L.conf) : a.conf;
+  int32_t* IDS = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.ids) : a.ids;
+  double* PROBS = a.stage ? reinterpret_cast<double*>(s_dyn + L.probs) : a.probs;
+  int32_t* ASG = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.asg) : a.assigned;
+  double* WT = a.stage ? reinterpret_cast<double*>(s_dyn + L.w) : a.weights;
+  uint8_t* IMP = s_dyn + L.imp;
+  const uint64_t all = expert_mask_all(N);
+  if (tid == 0) {
+    s_flags = 0;
+    s_nq = 0;
+    s_clipped = 0;
+  }
+  if (tid < N) s_icount[tid] = 0;
+  SEL_TS(0);
+  griddep_wait();  // logits come from K0 (programmatic dependent launch)
+  SEL_TS(1);
+
+  // 1) softmax + stable top-k + confidence, eight lanes per token.  Passes
+  // run whole warps (T rounded up to 4 tokens per warp) so shuffles converge.
+  const int Tw = (T + 3) & ~3;
+#pragma unroll 1
+  for (int t = grp; t < Tw; t += ngrp) {
+    const bool live = t < T;
+    double v[EPL];
+    if (a.logits) {
+      const double* z = a.logits + static_cast<size_t>(t) * N;
+      bool bad = false;
+      double m = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        const int e = j + 8 * q;
+        v[q] = e < N ? (live ? z[e] : 0.0) : -INFINITY;  // padding tokens route zeros
+        if (live && e < N) bad |= !isfinite(v[q]);
+        m = v[q] > m ? v[q] : m;
+      }
+      m = fmax(m, __shfl_xor_sync(kFull, m, 1));
+      m = fmax(m, __shfl_xor_sync(kFull, m, 2));
+      m = fmax(m, __shfl_xor_sync(kFull, m, 4));
+      SEL_TS_LOCAL(8);
+      if (bad) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? exp(v[q] - m) : 0.0;
+      SEL_TS_LOCAL(9);
+      const double sum = grp_pairwise<EPL>(v, N, j, gbase);
+      SEL_TS_LOCAL(10);
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) v[q] = v[q] / sum;  // e / s, as numpy divides
+      SEL_TS_LOCAL(11);
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < EPL; ++q)
+          if (j + 8 * q < N) {
+            P[static_cast<size_t>(t) * N + j + 8 * q] = v[q];
+            if (a.stage) a.full[static_cast<size_t>(t) * N + j + 8 * q] = v[q];
+          }
+      }
+      SEL_TS_LOCAL(12);
+      uint64_t taken = 0;
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+        double bv;
+        const int b = grp_best<EPL>(v, all & ~taken, j, &bv);
+        taken |= 1ull << b;
+        if (live && j == 0) {
+          IDS[t * k + r] = b;
+          PROBS[t * k + r] = bv;
+          if (a.stage) {
+            a.ids[t * k + r] = b;
+            a.probs[t * k + r] = bv;
+          }
+        }
+      }
+    } else {  // apply_policy on a given selection
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        const int e = j + 8 * q;
+        v[q] = (live && e < N) ? a.full[static_cast<size_t>(t) * N + e] : 0.0;
+        if (live && e < N) P[static_cast<size_t>(t) * N + e] = v[q];
+      }
+      if (live && j < k) {
+        IDS[t * k + j] = a.ids[t * k + j];
+        PROBS[t * k + j] = a.probs[t * k + j];
+      }
+    }
+    SEL_TS_LOCAL(13);
+    double top1;
+    const int first = grp_best<EPL>(v, all, j, &top1);
+    double c = top1;
+    if (a.pol.confidence_metric == LYNX_CONF_MARGIN) {
+      if (N == 1) {
+        c = grp_at<EPL>(v, 0, gbase);
+      } else {
+        double second;
+        grp_best<EPL>(v, all & ~(1ull << first), j, &second);
+        c = top1 - second;
+      }
+    }
+    if (live && j == 0) CONF[t] = c;
+  }
+  __syncthreads();
+  SEL_TS(2);
+
+  const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
+  const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
+  if (!run_policy) {
+    for (int e = tid; e < N; e += nthr) {
+      s_keep[e] = 1;
+      s_counts[e] = 0.0;
+    }
+    for (int t = tid; t < T; t += nthr) IMP[t] = 0;
+  } else {
+    batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
+  }
+  __syncthreads();
+  if (tid < 32) {  // retained bitmask: one ballot per 32 experts
+    const unsigned lo = __ballot_sync(kFull, tid < N && s_keep[tid]);
+    const unsigned hi = __ballot_sync(kFull, tid + 32 < N && s_keep[tid + 32]);
+    if (tid == 0) s_keepmask = (static_cast<unsigned long long>(hi) << 32) | lo;
+  }
+  __syncthreads();
+  SEL_TS(3);
+
+  // 2) remap onto the retained set (policy.py:171-210), or the identity
+  // mask with weights = probs / row sum (policy.py:215-229)
+  const uint64_t keep = s_keepmask;
+#pragma unroll 1
+  for (int t = grp; t < Tw; t += ngrp) {
+    const bool live = t < T;
+    double slot[LYNX_MAX_TOPK];
+    int asg[LYNX_MAX_TOPK];
+    if (run_policy) {
+      double v[EPL];
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        const int e = j + 8 * q;
+        v[q] = (live && e < N) ? P[static_cast<size_t>(t) * N + e] : 0.0;
+      }
+      int ids[LYNX_MAX_TOPK];
+      uint64_t occupied = 0;
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+        ids[r] = (live && r < k) ? IDS[t * k + r] : 0;
+        if (r < k && ((keep >> ids[r]) & 1ull)) occupied |= 1ull << ids[r];
+      }
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+        slot[r] = 0.0;
+        asg[r] = 0;
+        if (r < k) {  // shuffles stay warp-uniform: every group runs the arg-max
+          int e = ids[r];
+          double bv;
+          int pick = grp_best<EPL>(v, keep & ~occupied, j, &bv);
+          if (__any_sync(kFull, pick < 0)) {
+            const int any = grp_best<EPL>(v, keep, j, &bv);  // collapse (policy.py:197-200)
+            if (pick < 0) pick = any;
+          }
+          if (!((keep >> e) & 1ull)) {
+            e = pick;
+            occupied |= 1ull << e;
+          }
+          asg[r] = e;
+          slot[r] = grp_at<EPL>(v, e, gbase);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+        asg[r] = (live && r < k) ? IDS[t * k + r] : 0;
+        slot[r] = (live && r < k) ? PROBS[t * k + r] : 0.0;
+      }
+    }
+    if (live && j == 0) {
+      const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot, k);
+      if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r)
+        if (r < k) {
+          ASG[t * k + r] = asg[r];
+          WT[t * k + r] = slot[r] / total;
+        }
+    }
+  }
+  __syncthreads();
+  SEL_TS(4);
+
+  // 3) outputs
+  if (a.stage) {
+    for (int t = tid; t < T; t += nthr) a.conf[t] = CONF[t];
+    for (int i = tid; i < T * k; i += nthr) {
+      a.assigned[i] = ASG[i];
+      a.weights[i] = WT[i];
+    }
+  }
+  for (int e = tid; e < N; e += nthr) {
+    if (a.retained) a.retained[e] = static_cast<uint8_t>(s_keep[e]);
+    if (a.counts) a.counts[e] = s_counts[e];
+  }
+  if (a.important)
+    for (int t = tid; t < T; t += nthr) a.important[t] = accuracy ? IMP[t] : 0;
+  if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
+  SEL_TS(5);
+  if (a.plan.enabled)
+    plan_dispatch(ASG, WT, T, N, k, a.plan, reinterpret_cast<uint32_t*>(s_dyn + L.bits),
+                  reinterpret_cast<int*>(s_dyn + L.prefix));
+  SEL_TS(6);
+}
+
 // Dispatch plan from an assigned/weights mask in global memory (forward_layer path).
 __global__ void __launch_bounds__(kSelectThreads) plan_kernel(const int32_t* asg, const double* w, int T, int N,
-                                                              int k, PlanOut o) {
+                                                              int k, const __grid_constant__ PlanOut o) {
   extern __shared__ __align__(16) uint8_t s_dyn[];
   griddep_launch_dependents();
   griddep_wait();
@@ -963,6 +1312,17 @@ static cudaError_t allow_big_smem(const void* fn, int& configured_device) {
   return e;
 }
 
+// LYNX_SELECT_WARP=1 forces the warp-per-token kernel for N > 16 (A/B and
+// cross-check of the group path).
+static bool group_path_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LYNX_SELECT_WARP");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
   const size_t smem = select_smem_bytes(a.T, a.N, a.k, a.stage, a.plan.enabled);
   if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
@@ -987,6 +1347,22 @@ cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
       if (e != cudaSuccess) return e;
     }
     return launch_pdl(route_select_fast<16>, dim3(1), dim3(threads), smem, s, a);
+  }
+  // Group path: 16 < N <= 64, eight lanes per token.
+  if (group_path_enabled()) {
+    static int configured32 = -1, configured64 = -1;
+    if (a.N <= 32) {
+      if (smem > 48 * 1024) {
+        cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<4>), configured32);
+        if (e != cudaSuccess) return e;
+      }
+      return launch_pdl(route_select_group<4>, dim3(1), dim3(kSelectThreads), smem, s, a);
+    }
+    if (smem > 48 * 1024) {
+      cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<8>), configured64);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_pdl(route_select_group<8>, dim3(1), dim3(kSelectThreads), smem, s, a);
   }
   return launch_pdl(route_select_kernel, dim3(1), dim3(kSelectThreads), smem, s, a);
 }

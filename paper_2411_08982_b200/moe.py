@@ -87,6 +87,7 @@ class MoEWeights:
             L = nat.LynxLayer()
             L.num_experts, L.top_k, L.d_model, L.d_ff = s.num_experts, s.top_k, s.d_model, s.d_ff
             L.activation = ACTIVATIONS[self.activation]
+            L.num_shared = s.num_shared_experts
             L.w13 = nat.ptr(self.w13[layer])
             L.w2 = nat.ptr(self.w2[layer])
             L.router_wt = nat.ptr(self.router_wt[layer]) if self.router_wt[layer] is not None else 0
@@ -102,21 +103,23 @@ class MoEWeights:
 def build_swiglu_model(spec: MoEModelSpec, seed: int = 0, router_gain: float = 2.0,
                        device: str = "cuda") -> MoEWeights:
     """Random-init SwiGLU stack (SURVEY 8d recipe, after simulator.py:44-74):
-    router ~ N(0, (gain/sqrt(d))^2), W1, W3 ~ N(0, 1/d), W2 ~ N(0, 1/ff); bf16."""
+    router ~ N(0, (gain/sqrt(d))^2), W1, W3 ~ N(0, 1/d), W2 ~ N(0, 1/ff); bf16.
+    Shared experts (spec.num_shared_experts) are experts N..N+S-1 of w13/w2."""
     torch = _torch()
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     N, d, ff = spec.num_experts, spec.d_model, spec.d_ff
+    E = N + spec.num_shared_experts
     w13s, w2s, routers = [], [], []
     for _ in range(spec.num_layers):
-        w13 = torch.randn((N, swiglu_rows(ff), d), generator=g, device=device, dtype=torch.bfloat16)
+        w13 = torch.randn((E, swiglu_rows(ff), d), generator=g, device=device, dtype=torch.bfloat16)
         w13.mul_(1.0 / np.sqrt(d))
         if ff % 64:  # zero the padding features of the packed layout
             f = torch.arange(ff, swiglu_rows(ff) // 2)
             for up in (False, True):
                 rows = 128 * (f // 64) + 32 * ((f % 64) // 16) + (16 if up else 0) + f % 16
                 w13[:, rows.to(device)] = 0
-        w2 = torch.randn((N, d, ff), generator=g, device=device, dtype=torch.bfloat16)
+        w2 = torch.randn((E, d, ff), generator=g, device=device, dtype=torch.bfloat16)
         w2.mul_(1.0 / np.sqrt(ff))
         r = torch.randn((N, d), generator=g, device=device, dtype=torch.bfloat16)
         r.mul_(router_gain / np.sqrt(d))
@@ -291,6 +294,37 @@ class LynxMoELayer:
         nat.check(st, "lynx_moe_layer")
         return out
 
+    def host_step(self, hidden_host, out_host):
+        """One decode-layer step on PINNED HOST buffers: host->device copy of
+        ``hidden_host`` [T, d] bf16, the layer (K0..K4), device->host copy into
+        ``out_host``.  The three are captured once per buffer pair into a CUDA
+        graph and replayed on the current stream, so a step costs one graph
+        launch.  Returns ``out_host``; it is valid after the stream syncs."""
+        torch = _torch()
+        d = self.model.spec.d_model
+        for t in (hidden_host, out_host):
+            if t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != (self.T, d) or not t.is_pinned():
+                raise ValidationError(f"host_step takes pinned host bf16 tensors of shape [{self.T}, {d}]")
+        key = (hidden_host.data_ptr(), out_host.data_ptr())
+        graphs = self.__dict__.setdefault("_host_graphs", {})
+        if key not in graphs:
+            dev_in = torch.empty((self.T, d), dtype=torch.bfloat16, device="cuda")
+            dev_out = torch.empty_like(dev_in)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):  # warm-up outside capture (lazy init, TMA descriptors)
+                dev_in.copy_(hidden_host, non_blocking=True)
+                self(dev_in, dev_out)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                dev_in.copy_(hidden_host, non_blocking=True)
+                self(dev_in, dev_out)
+                out_host.copy_(dev_out, non_blocking=True)
+            graphs[key] = (g, dev_in, dev_out)
+        graphs[key][0].replay()
+        return out_host
+
     def profiled(self, hidden, events, out=None):
         """__call__ that records 6 torch.cuda.Events around K0..K4 (lynx_moe_layer_profiled)."""
         torch = _torch()
@@ -311,10 +345,12 @@ class LynxMoELayer:
         return out
 
     def used_experts(self) -> int:
-        """Experts with >= 1 assigned slot in the last call (host sync; reporting only)."""
+        """Experts streamed by the last call: routed experts with >= 1 assigned
+    slot plus the shared experts (host sync; reporting only)."""
         torch = _torch()
-        N = self.model.spec.num_experts
-        return int((torch.bincount(self.assigned.flatten().long(), minlength=N) > 0).sum().item())
+        s = self.model.spec
+        used = torch.bincount(self.assigned.flatten().long(), minlength=s.num_experts) > 0
+        return int(used.sum().item()) + s.num_shared_experts
 
     def mask(self) -> ExpertMask:
         """The last call's ExpertMask (host sync)."""

@@ -39,6 +39,9 @@ class MoEModelSpec:
     d_model: int
     d_ff: int
     bytes_per_param: int = 2
+    # Builder extension (not in the reference): always-on shared experts of
+    # size d_ff applied to every token with weight 1 (DeepSeek-MoE).
+    num_shared_experts: int = 0
 
     def __post_init__(self) -> None:
         if self.num_layers < 1:
@@ -52,6 +55,8 @@ class MoEModelSpec:
             raise ValidationError("d_model and d_ff must be >= 1")
         if self.bytes_per_param < 1:
             raise ValidationError("bytes_per_param must be >= 1")
+        if not (0 <= self.num_shared_experts <= nat.MAX_SHARED):
+            raise ValidationError(f"num_shared_experts must be in [0, {nat.MAX_SHARED}]")
 
     @property
     def expert_param_bytes(self) -> int:

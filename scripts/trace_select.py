@@ -18,10 +18,14 @@ PHASES = ["start->griddep_wait", "wait", "route(softmax/topk/conf)", "policy", "
 def main():
     lib = nat.lib()
     lib.lynx_debug_select_ts.argtypes = [ctypes.c_void_p]
-    T, N, k, d, ff = 32, 8, 2, 4096, 14336
-    spec = L.MoEModelSpec(2, N, k, d, ff)
+    if "--c4" in sys.argv:  # DeepSeek-MoE-16B shape, accuracy policy
+        T, N, k, d, ff, S = 128, 64, 6, 2048, 1408, 2
+        cfg = L.PolicyConfig(mode="accuracy", freq_keep_budget=16)
+    else:
+        T, N, k, d, ff, S = 32, 8, 2, 4096, 14336, 0
+        cfg = L.PolicyConfig(mode="latency", drop_count=4)
+    spec = L.MoEModelSpec(2, N, k, d, ff, num_shared_experts=S)
     model = L.build_swiglu_model(spec, seed=0)
-    cfg = L.PolicyConfig(mode="latency", drop_count=4)
     layers = [L.LynxMoELayer(model, l, T, policy=cfg) for l in range(2)]
     h = torch.randn((T, d), device="cuda").to(torch.bfloat16)
     res = {}
@@ -40,6 +44,10 @@ def main():
             lib.lynx_debug_select_ts(buf.ctypes.data)
             ts = buf[:7].astype(np.int64)
             rows.append(np.diff(ts) / 1e3)
+            if buf[8]:  # group path sub-phases (warp 0's own timeline)
+                sub = buf[[1, 8, 9, 10, 11, 12, 13]].astype(np.int64)
+                print(label, "route sub-phases (us): load+max, exp, sum, div, write, topk:",
+                      np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
         m = np.median(np.array(rows), axis=0)
         res[label] = {p: round(float(v), 2) for p, v in zip(PHASES[1:], m)}
         res[label]["total_us"] = round(float(m.sum()), 2)

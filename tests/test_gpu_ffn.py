@@ -42,8 +42,9 @@ def make_mask(T, N, k, seed, drop=None):
 def oracle_swiglu(model, layer, hidden_bf16, mask):
     w1, w3 = L.unpack_w13(model.w13[layer], model.spec.d_ff)
     f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    N, S = model.spec.num_experts, model.spec.num_shared_experts
     return O.forward_swiglu(f(hidden_bf16), f(w1), f(w3), f(model.w2[layer]), _np(mask.remap_assigned).astype(np.int64),
-                            _np(mask.remap_weights), round_h_bf16=True)
+                            _np(mask.remap_weights), round_h_bf16=True, shared=range(N, N + S))
 
 
 def test_permute_order_matches_reference_dispatch():
@@ -177,3 +178,62 @@ def test_mixtral_shape_layer_vs_oracle():
     ref = oracle_swiglu(model, 0, hidden, mask)
     assert O.norm_rel_err(_np(y), ref) <= TOL
     assert O.norm_rel_err(_np(y) - _np(hidden), ref - _np(hidden)) <= 3 * TOL
+
+
+@pytest.mark.parametrize("T,N,k,S,d,ff", [
+    (16, 8, 2, 1, 128, 256),     # one shared expert
+    (37, 16, 4, 2, 256, 192),    # T not a multiple of 16 (padded shared segment)
+    (300, 8, 2, 2, 128, 128),    # shared segments split at 256 rows
+])
+def test_forward_shared_experts_vs_oracle(T, N, k, S, d, ff):
+    """Always-on shared experts (DeepSeek-MoE, builder extension): every token,
+    weight 1, after the routed experts."""
+    spec = L.MoEModelSpec(1, N, k, d, ff, num_shared_experts=S)
+    model = L.build_swiglu_model(spec, seed=T + S)
+    mask = make_mask(T, N, k, seed=T)
+    hidden = torch.randn((T, d), device="cuda").to(torch.bfloat16)
+    y = L.forward_layer(hidden, model, 0, mask)
+    ref = oracle_swiglu(model, 0, hidden, mask)
+    assert O.norm_rel_err(_np(y), ref) <= TOL
+    assert O.norm_rel_err(_np(y) - _np(hidden), ref - _np(hidden)) <= 3 * TOL
+
+
+def test_deepseek_shape_layer_vs_oracle():
+    """C4: DeepSeek-MoE-16B layer shape (64 routed + 2 shared, top-6, d=2048,
+    ff=1408), T=128, Lynx accuracy policy (dynamic selection), vs fp32 oracle;
+    the selection is checked bit-exactly against the oracle on the kernel's logits."""
+    spec = L.MoEModelSpec(1, 64, 6, 2048, 1408, num_shared_experts=2)
+    model = L.build_swiglu_model(spec, seed=0)
+    T = 128
+    g = torch.Generator(device="cuda").manual_seed(0)
+    hidden = torch.randn((T, 2048), generator=g, device="cuda").to(torch.bfloat16)
+    cfg = L.PolicyConfig(mode="accuracy", freq_keep_budget=16)
+    layer = L.LynxMoELayer(model, 0, T, policy=cfg)
+    y = layer(hidden)
+    mask = layer.mask()
+    logits = _np(L.router_logits(model, 0, hidden))
+    ids, probs, full = O.route(logits, 6)
+    ref_mask = O.apply(ids, probs, full, O.Policy(mode="accuracy", freq_keep_budget=16))
+    assert np.array_equal(_np(layer.expert_ids), ids)
+    assert np.array_equal(_np(mask.retained), ref_mask.retained)
+    assert np.array_equal(_np(layer.assigned), ref_mask.assigned)
+    ref = oracle_swiglu(model, 0, hidden, mask)
+    assert O.norm_rel_err(_np(y), ref) <= TOL
+    assert O.norm_rel_err(_np(y) - _np(hidden), ref - _np(hidden)) <= 3 * TOL
+    assert layer.used_experts() == len(np.unique(ref_mask.assigned)) + 2
+
+
+def test_host_step_graph_matches_device_call():
+    """LynxMoELayer.host_step (H2D + layer + D2H replayed as one CUDA graph)
+    returns exactly what the device-resident call returns, step after step."""
+    spec = L.MoEModelSpec(1, 8, 2, 256, 512)
+    model = L.build_swiglu_model(spec, seed=2)
+    layer = L.LynxMoELayer(model, 0, 24, policy=L.PolicyConfig(mode="latency", drop_count=3))
+    h_host = torch.randn((24, 256)).to(torch.bfloat16).pin_memory()
+    o_host = torch.empty_like(h_host).pin_memory()
+    for step in range(3):
+        h_host.copy_(torch.randn((24, 256)).to(torch.bfloat16))  # new input, same pinned buffer
+        layer.host_step(h_host, o_host)
+        torch.cuda.synchronize()
+        ref = layer(h_host.cuda()).cpu()
+        assert torch.equal(o_host, ref), step

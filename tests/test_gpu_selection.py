@@ -116,7 +116,11 @@ def test_remap_golden(remap_golden):
         assert close(_np(w), c["weights"]), i
 
 
-@pytest.mark.parametrize("shape", [(16, 8, 2), (32, 8, 2), (128, 64, 6), (256, 8, 2), (1000, 16, 4)])
+@pytest.mark.parametrize("shape", [(16, 8, 2), (32, 8, 2), (128, 64, 6), (256, 8, 2), (1000, 16, 4),
+                                   # group path (16 < N <= 64): partial warps, several passes, odd N
+                                   (1, 17, 1), (3, 20, 3), (130, 33, 5), (64, 64, 8), (300, 48, 4),
+                                   # rows too large to stage in shared memory (global working arrays)
+                                   (4096, 8, 2), (2000, 64, 6)])
 def test_random_sweep_vs_oracle(shape):
     """Seeded sweeps at the BASELINE shapes (fp32-valued logits as K0 produces)."""
     T, N, k = shape
