@@ -65,6 +65,7 @@ enum lynx_status {
 #define LYNX_MAX_EXPERTS 64
 #define LYNX_MAX_TOPK 8
 #define LYNX_MAX_SHARED 4         /* always-on shared experts per layer (DeepSeek-MoE style) */
+#define LYNX_MAX_DHEAD 64         /* attention stand-in head width */
 #define LYNX_MAX_TOKENS 4096
 #define LYNX_SEG_ROWS 256        /* max token rows one expert segment feeds one MMA */
 
@@ -216,6 +217,57 @@ int lynx_moe_layer_profiled(const lynx_layer_t *layer, const uint16_t *hidden, i
  * interleaved w13 layout the SwiGLU kernel streams. */
 int lynx_pack_w13(const uint16_t *w1, const uint16_t *w3, int N, int ff, int d, uint16_t *w13,
                   lynx_stream_t stream);
+
+/* ---- decode stack around the layer -------------------
+ * The reference model's single-head attention stand-in plus its residual,
+ * h_out = h + attention(layer, h)  (simulator.py:308-326, 333), with a
+ * per-layer KV cache.  A chunk of Tn new tokens per sequence (B sequences;
+ * rows b*Tn+i of h_in/h_out) occupies cache positions *pos .. *pos+Tn-1 and
+ * attends causally (simulator.py:318-321).  `pos` is device memory so a
+ * captured decode step replays step after step; lynx_advance_position adds
+ * `by` to it on the stream.  norm_input = 1 feeds rms_norm(h_in) as the
+ * layer input (the decode step's rms_norm(prev), simulator.py:353). */
+typedef struct lynx_attention {
+  int32_t d_model;          /* d (multiple of 8) */
+  int32_t d_head;           /* dh <= LYNX_MAX_DHEAD */
+  int32_t max_len;          /* cache capacity in positions */
+  int32_t reserved;
+  const uint16_t *wqkv;     /* [3*dh, d] bf16: wq^T, wk^T, wv^T (reference [d, dh] each, simulator.py:35-37) */
+  const uint16_t *wo;       /* [dh, d] bf16 (reference wo, simulator.py:38) */
+  float *k_cache;           /* [B, max_len, dh] f32 */
+  float *v_cache;           /* [B, max_len, dh] f32 */
+} lynx_attention_t;
+
+size_t lynx_attention_workspace_bytes(int rows, int d_head);
+int lynx_attention(const lynx_attention_t *attn, const uint16_t *h_in, int B, int Tn, int norm_input,
+                   const int32_t *pos, uint16_t *h_out, void *workspace, size_t workspace_bytes,
+                   lynx_stream_t stream);
+int lynx_advance_position(int32_t *pos, int by, lynx_stream_t stream);
+
+/* ---- device trace ring -------------------------------
+ * Routing events of a captured decode step are appended on the device, so
+ * tracing costs no host sync per step; the host later serialises the ring
+ * into the reference's trace JSONL (trace.py:24-35, 81-125).  Slot =
+ * (*pos) % capacity, the slot's cache position goes to positions[slot].
+ * conf is the top-1 confidence the reference traces (trace.py:90). */
+typedef struct lynx_trace_ring {
+  int32_t capacity;       /* steps held */
+  int32_t num_layers;     /* L */
+  int32_t T, k, N, reserved;
+  int32_t *positions;     /* [cap] */
+  int32_t *original;      /* [cap, L, T, k] remap_original */
+  int32_t *assigned;      /* [cap, L, T, k] remap_assigned */
+  double *weights;        /* [cap, L, T, k] remap_weights */
+  double *conf;           /* [cap, L, T]    top-1 confidence */
+  uint8_t *retained;      /* [cap, L, N] */
+  uint8_t *important;     /* [cap, L, T] */
+  int32_t *flags;         /* [cap, L]       LYNX_FLAG_* */
+} lynx_trace_ring_t;
+
+/* sel: the layer's selection outputs (expert_ids, full_probs, assigned,
+ * weights, retained, important, flags must be set). */
+int lynx_trace_append(const lynx_trace_ring_t *ring, const int32_t *pos, int layer,
+                      const lynx_selection_t *sel, lynx_stream_t stream);
 
 /* ---- expert parallel helpers -------------------------
  * Rank r of G owns experts [r*N/G, (r+1)*N/G).  Dispatch rows are sent with

@@ -425,3 +425,61 @@ def norm_rel_err(y, y_ref) -> float:
     y = np.asarray(y, dtype=np.float64)
     y_ref = np.asarray(y_ref, dtype=np.float64)
     return float(np.max(np.abs(y - y_ref)) / max(np.max(np.abs(y_ref)), 1e-30))
+
+
+# --------------------------------------------------------------------------
+# decode stack around the layer (simulator.py:273-357)
+# --------------------------------------------------------------------------
+
+def attention(h, wq, wk, wv, wo, keys, vals, offset):
+    """The single-head attention stand-in (simulator.py:308-326) for one layer.
+
+    h [B, Tn, d]; wq/wk/wv [d, dh]; wo [dh, d]; keys/vals [B, S, dh] hold the
+    S cached positions.  The chunk sits at positions offset .. offset+Tn-1
+    and attends causally.  Returns (attention output [B, Tn, d], keys, vals)
+    with the chunk's k/v appended -- the caller adds the residual
+    (simulator.py:333).
+    """
+    h = np.asarray(h, dtype=np.float64)
+    xn = rms_norm(h)
+    q = xn @ wq
+    keys = np.concatenate([keys, xn @ wk], axis=1)
+    vals = np.concatenate([vals, xn @ wv], axis=1)
+    scores = np.einsum("bth,bsh->bts", q, keys) / np.sqrt(wq.shape[1])
+    total, t_new = keys.shape[1], h.shape[1]
+    allowed = np.arange(total)[None, :] <= (offset + np.arange(t_new))[:, None]
+    scores = np.where(allowed[None], scores, -np.inf)
+    a = np.exp(scores - scores.max(axis=-1, keepdims=True))
+    a = a / a.sum(axis=-1, keepdims=True)
+    return np.einsum("bts,bsh->bth", a, vals) @ wo, keys, vals
+
+
+def simulate(inputs, decode_steps, num_layers, attn_weights, moe_layer):
+    """simulate() (simulator.py:273-357) with a pluggable MoE sublayer.
+
+    attn_weights[l] = (wq, wk, wv, wo); moe_layer(l, phase, flat [T, d]) ->
+    flat output ("prefill" / "decode").  Returns hidden [B, P + D, d].
+    """
+    x = np.asarray(inputs, dtype=np.float64)
+    B, P, d = x.shape
+    dh = attn_weights[0][0].shape[1]
+    keys = [np.zeros((B, 0, dh)) for _ in range(num_layers)]
+    vals = [np.zeros((B, 0, dh)) for _ in range(num_layers)]
+    out = np.zeros((B, P + decode_steps, d))
+
+    def chunk(h, phase, offset):
+        for l in range(num_layers):
+            a, keys[l], vals[l] = attention(h, *attn_weights[l], keys[l], vals[l], offset)
+            h = h + a
+            Bc, Tc, _ = h.shape
+            h = moe_layer(l, phase, h.reshape(Bc * Tc, d)).reshape(Bc, Tc, d)
+        return h
+
+    h = chunk(x, "prefill", 0)
+    out[:, :P] = h
+    prev = h[:, -1]
+    for s in range(decode_steps):
+        h = chunk(rms_norm(prev)[:, None, :], "decode", P + s)
+        out[:, P + s] = h[:, 0]
+        prev = h[:, 0]
+    return out

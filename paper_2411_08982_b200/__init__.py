@@ -9,6 +9,7 @@ moetrim/__init__.py:35-73 for this path.
 
 from ._version import __version__
 from .errors import NativeLibraryError, TraceFormatError, ValidationError
+from .decode import AttentionWeights, DecodeStack, SimResult, attention_from_reference, build_attention
 from .moe import (
     LynxMoELayer,
     MoEWeights,
@@ -45,7 +46,21 @@ from .router import (
     top_k_select,
 )
 
+from .trace import (
+    MaskRecord,
+    TraceRecord,
+    TraceRecorder,
+    masks_path_for,
+    read_masks_jsonl,
+    read_trace_jsonl,
+    write_masks_jsonl,
+    write_trace_jsonl,
+)
+
 __all__ = [
+    "AttentionWeights", "DecodeStack", "SimResult", "attention_from_reference", "build_attention",
+    "MaskRecord", "TraceRecord", "TraceRecorder", "masks_path_for", "read_masks_jsonl", "read_trace_jsonl",
+    "write_masks_jsonl", "write_trace_jsonl",
     "__version__", "NativeLibraryError", "TraceFormatError", "ValidationError",
     "LynxMoELayer", "MoEWeights", "build_swiglu_model", "forward_layer", "forward_partial",
     "from_hf_swiglu", "from_reference", "pack_w13", "router_logits", "unpack_w13",

@@ -26,7 +26,7 @@ STATUS = {
 }
 VALIDATION_CODES = {-1, -2, -3, -4, -5, -7, -9}
 FLAG_CLIPPED, FLAG_NONFINITE, FLAG_ZERO_MASS = 1, 2, 4
-MAX_EXPERTS, MAX_TOPK, MAX_TOKENS, SEG_ROWS, MAX_SHARED = 64, 8, 4096, 256, 4
+MAX_EXPERTS, MAX_TOPK, MAX_TOKENS, SEG_ROWS, MAX_SHARED, MAX_DHEAD = 64, 8, 4096, 256, 4, 64
 POLICY_NONE, POLICY_LATENCY, POLICY_ACCURACY = 0, 1, 2
 CONF_TOP1, CONF_MARGIN = 0, 1
 ACT_SWIGLU, ACT_TANH2 = 0, 1
@@ -56,6 +56,18 @@ class LynxLayer(ctypes.Structure):
                 ("w13", _p), ("w2", _p), ("router_wt", _p)]
 
 
+class LynxAttention(ctypes.Structure):
+    _fields_ = [("d_model", ctypes.c_int32), ("d_head", ctypes.c_int32), ("max_len", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("wqkv", _p), ("wo", _p), ("k_cache", _p), ("v_cache", _p)]
+
+
+class LynxTraceRing(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_int32), ("num_layers", ctypes.c_int32), ("T", ctypes.c_int32),
+                ("k", ctypes.c_int32), ("N", ctypes.c_int32), ("reserved", ctypes.c_int32)] + [
+        (name, _p) for name in ("positions", "original", "assigned", "weights", "conf", "retained", "important",
+                                "flags")]
+
+
 class LynxDispatch(ctypes.Structure):
     _fields_ = [(name, _p) for name in (
         "n_seg", "n_used", "n_rows", "seg_expert", "seg_row", "seg_count", "perm_token", "perm_weight",
@@ -79,6 +91,10 @@ _SIGS = {
     "lynx_moe_layer": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_layer_profiled": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p, _p, _i]),
     "lynx_pack_w13": (_i, [_p, _p, _i, _i, _i, _p, _p]),
+    "lynx_attention_workspace_bytes": (ctypes.c_size_t, [_i, _i]),
+    "lynx_attention": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, ctypes.c_size_t, _p]),
+    "lynx_advance_position": (_i, [_p, _i, _p]),
+    "lynx_trace_append": (_i, [_p, _p, _i, _p, _p]),
     "lynx_ep_pack": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "lynx_ep_local_mask": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p]),
     "lynx_ep_combine": (_i, [_p, _p, _i, _i, _i, _p, _p]),

@@ -581,6 +581,56 @@ int lynx_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, 
   return cuda_status(launch_pack_w13(w1, w3, N, ff, d, w13, stream));
 }
 
+size_t lynx_attention_workspace_bytes(int rows, int d_head) {
+  if (rows < 1 || d_head < 1) return 0;
+  return sizeof(float) * static_cast<size_t>(rows) * d_head + 256;
+}
+
+int lynx_attention(const lynx_attention_t* attn, const uint16_t* h_in, int B, int Tn, int norm_input,
+                   const int32_t* pos, uint16_t* h_out, void* workspace, size_t workspace_bytes,
+                   lynx_stream_t stream) {
+  if (!attn || !h_in || !h_out || !pos || B < 1 || Tn < 1) return LYNX_ERR_SHAPE;
+  if (attn->d_model < 8 || attn->d_head < 1 || attn->max_len < Tn) return LYNX_ERR_SHAPE;
+  if (!attn->wqkv || !attn->wo || !attn->k_cache || !attn->v_cache) return LYNX_ERR_SHAPE;
+  if (attn->d_model % 8 || attn->d_head > LYNX_MAX_DHEAD ||
+      attn_out_smem(attn->d_model, attn->d_head, attn->max_len) > 200 * 1024)
+    return LYNX_ERR_UNSUPPORTED;
+  if (!workspace || workspace_bytes < lynx_attention_workspace_bytes(B * Tn, attn->d_head)) return LYNX_ERR_WORKSPACE;
+  AttnArgs a;
+  a.h_in = h_in;
+  a.wqkv = attn->wqkv;
+  a.wo = attn->wo;
+  a.kcache = attn->k_cache;
+  a.vcache = attn->v_cache;
+  a.q = static_cast<float*>(aligned_ws(workspace));
+  a.pos = pos;
+  a.B = B;
+  a.Tn = Tn;
+  a.d = attn->d_model;
+  a.dh = attn->d_head;
+  a.max_len = attn->max_len;
+  a.norm_input = norm_input ? 1 : 0;
+  a.h_out = h_out;
+  return cuda_status(launch_attention(a, stream));
+}
+
+int lynx_advance_position(int32_t* pos, int by, lynx_stream_t stream) {
+  if (!pos) return LYNX_ERR_SHAPE;
+  return cuda_status(launch_advance_position(pos, by, stream));
+}
+
+int lynx_trace_append(const lynx_trace_ring_t* ring, const int32_t* pos, int layer, const lynx_selection_t* sel,
+                      lynx_stream_t stream) {
+  if (!ring || !pos || !sel || ring->capacity < 1 || layer < 0 || layer >= ring->num_layers) return LYNX_ERR_SHAPE;
+  if (ring->T < 1 || ring->k < 1 || ring->N < 1) return LYNX_ERR_SHAPE;
+  if (!ring->positions || !ring->original || !ring->assigned || !ring->weights || !ring->conf || !ring->retained ||
+      !ring->important || !ring->flags)
+    return LYNX_ERR_SHAPE;
+  if (!sel->expert_ids || !sel->full_probs || !sel->assigned || !sel->weights || !sel->retained || !sel->flags)
+    return LYNX_ERR_SHAPE;
+  return cuda_status(launch_trace_append(*ring, pos, layer, *sel, stream));
+}
+
 int lynx_ep_pack(const uint16_t* hidden_local, const int32_t* assigned, int T_local, int k, int N, int G, int d,
                  int rank, uint16_t* send, lynx_stream_t stream) {
   if (T_local < 1 || G < 1 || N % G || rank < 0 || rank >= G || d % 8) return LYNX_ERR_SHAPE;

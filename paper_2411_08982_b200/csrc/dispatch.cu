@@ -112,6 +112,51 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s) {
   return launch_pdl(combine_kernel, dim3((a.d + 511) / 512, a.T), dim3(128), 0, s, a);
 }
 
+// ------------------------------------------------------------ trace ring
+// Copy one layer's routing event into the device ring at slot (*pos) % cap.
+struct TraceAppendArgs {
+  lynx_trace_ring_t r;
+  const int32_t* pos;
+  int layer;
+  lynx_selection_t sel;
+};
+
+__global__ void __launch_bounds__(256) trace_append_kernel(const __grid_constant__ TraceAppendArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const lynx_trace_ring_t& r = a.r;
+  const int p = *a.pos;
+  const int slot = p % r.capacity;
+  const size_t ev = static_cast<size_t>(slot) * r.num_layers + a.layer;
+  const int T = r.T, k = r.k, N = r.N;
+  for (int i = threadIdx.x; i < T * k; i += blockDim.x) {
+    r.original[ev * T * k + i] = a.sel.expert_ids[i];
+    r.assigned[ev * T * k + i] = a.sel.assigned[i];
+    r.weights[ev * T * k + i] = a.sel.weights[i];
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    double m = a.sel.full_probs[static_cast<size_t>(t) * N];
+    for (int e = 1; e < N; ++e) m = fmax(m, a.sel.full_probs[static_cast<size_t>(t) * N + e]);
+    r.conf[ev * T + t] = m;
+    r.important[ev * T + t] = a.sel.important ? a.sel.important[t] : 0;
+  }
+  for (int e = threadIdx.x; e < N; e += blockDim.x) r.retained[ev * N + e] = a.sel.retained[e];
+  if (threadIdx.x == 0) {
+    r.flags[ev] = a.sel.flags[0];
+    if (a.layer == 0) r.positions[slot] = p;
+  }
+}
+
+cudaError_t launch_trace_append(const lynx_trace_ring_t& r, const int32_t* pos, int layer,
+                                const lynx_selection_t& sel, cudaStream_t s) {
+  TraceAppendArgs a;
+  a.r = r;
+  a.pos = pos;
+  a.layer = layer;
+  a.sel = sel;
+  return launch_pdl(trace_append_kernel, dim3(1), dim3(256), 0, s, a);
+}
+
 // --------------------------------------------------------------- packing
 // w13 row r of expert e: tile = r/128, q = (r%128)/32, half = (r%32)/16,
 // i = r%16 -> feature f = 64*tile + 16*q + i of w1 (half 0) or w3 (half 1).

@@ -120,6 +120,25 @@ struct GatherArgs {
   uint16_t* x_perm;
 };
 
+// Attention stand-in (attention.cu).
+struct AttnArgs {
+  const uint16_t* h_in;  // [B*Tn, d]
+  const uint16_t* wqkv;  // [3*dh, d]
+  const uint16_t* wo;    // [dh, d]
+  float* kcache;         // [B, max_len, dh]
+  float* vcache;
+  float* q;              // [B*Tn, dh] scratch
+  const int32_t* pos;
+  int B, Tn, d, dh, max_len, norm_input;
+  uint16_t* h_out;
+};
+size_t attn_out_smem(int d, int dh, int max_len);
+cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
+cudaError_t launch_advance_position(int32_t* pos, int by, cudaStream_t s);
+
+cudaError_t launch_trace_append(const lynx_trace_ring_t& r, const int32_t* pos, int layer,
+                                const lynx_selection_t& sel, cudaStream_t s);
+
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s);
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan);

@@ -243,7 +243,7 @@ class LynxMoELayer:
     """
 
     def __init__(self, model: MoEWeights, layer_index: int, num_tokens: int,
-                 policy: PolicyConfig | None = None, phase: Phase = Phase.DECODE):
+                 policy: PolicyConfig | None = None, phase: Phase = Phase.DECODE, workspace=None):
         torch = _torch()
         s = model.spec
         self.model, self.layer_index, self.T = model, layer_index, int(num_tokens)
@@ -256,7 +256,10 @@ class LynxMoELayer:
             self._pol = None
         self._layer = model.native_layer(layer_index)
         nbytes = int(nat.lib().lynx_moe_workspace_bytes(ctypes_ref(self._layer), self.T))
-        self.workspace = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+        if workspace is not None and workspace.numel() >= nbytes:
+            self.workspace = workspace  # shared by layers that run in stream order
+        else:
+            self.workspace = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
         T, N, k = self.T, s.num_experts, s.top_k
         dev = "cuda"
         self.expert_ids = torch.empty((T, k), dtype=torch.int32, device=dev)
