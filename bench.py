@@ -41,6 +41,10 @@ CONFIGS = {
                       mode="latency", drop=0, rotate=4),
     "c2-acc": dict(workload="mixtral-8x7b-moe-layer-decode-bs32-lynx-accuracy", d=4096, ff=14336, N=8, k=2,
                    T=32, mode="accuracy", drop=0, rotate=4),
+    # configs[2]: Mixtral-8x7B full 32-layer decode step (attention stand-in + MoE layer per layer, one CUDA
+    # graph per step), batch 64, kept-expert budget swept 8 -> 4 (latency policy drop 0..4); headline = budget 4
+    "c3": dict(workload="mixtral-8x7b-32-layer-decode-step-bs64-lynx-latency-budget-sweep", d=4096, ff=14336, N=8,
+               k=2, T=64, layers=32, mode="latency", drop=4, sweep=(0, 1, 2, 3, 4), prefill=16, d_head=16),
     # configs[3]: DeepSeek-MoE-16B shape, 64 routed + 2 shared experts, top-6, dynamic (accuracy) selection
     "c4": dict(workload="deepseek-moe-16b-layer-decode-bs128-lynx-accuracy-budget16", d=2048, ff=1408, N=64, S=2,
                k=6, T=128, mode="accuracy", drop=0, budget=16, rotate=6),
@@ -182,10 +186,13 @@ def cpu_baseline(c, steps=3):
     for i in range(steps):
         cpu_layer_step(st, i)
     dt = (time.perf_counter() - t0) / steps
-    return {"value": c["T"] / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
-            "sample": f"{steps} full layer steps (T={c['T']}, router+route+{c['mode']} policy+SwiGLU fp32 over "
-                      f"the used experts) of the oracle port oracle/lynx_oracle.py, numpy/OpenBLAS",
-            "ms_per_step": dt * 1e3}
+    nl = c.get("layers", 1)
+    sample = (f"{steps} full layer steps (T={c['T']}, router+route+{c['mode']} policy+SwiGLU fp32 over "
+              f"the used experts) of the oracle port oracle/lynx_oracle.py, numpy/OpenBLAS")
+    if nl > 1:
+        sample += f"; the {nl}-layer step is timed as {nl} x one layer (attention stand-in not included)"
+    return {"value": c["T"] / (dt * nl), "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+            "sample": sample, "ms_per_step": dt * 1e3 * nl}
 
 
 # -------------------------------------------------------------- reference arm
@@ -199,7 +206,7 @@ def run_reference(args, c):
     t0 = time.perf_counter()
     for i in range(args.steps):
         cpu_layer_step(st, i)
-    dt = (time.perf_counter() - t0) / args.steps
+    dt = (time.perf_counter() - t0) / args.steps * c.get("layers", 1)  # C3: layers x one layer step
     value = c["T"] / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
@@ -331,6 +338,89 @@ def run_single(args, c):
     return result
 
 
+def run_stack(args, c):
+    """C3: the full decode step (simulate's decode loop, simulator.py:351-355) over
+    all layers, replayed as one CUDA graph per step, for each kept-expert budget."""
+    import torch
+
+    import paper_2411_08982_b200 as L
+    B, d, ff, N, k, nl = c["T"], c["d"], c["ff"], c["N"], c["k"], c["layers"]
+    spec = L.MoEModelSpec(num_layers=nl, num_experts=N, top_k=k, d_model=d, d_ff=ff)
+    model = L.build_swiglu_model(spec, seed=0)
+    attn = L.build_attention(nl, d, c["d_head"], seed=1)
+    P = c["prefill"]
+    x = torch.randn((B, P, d), generator=torch.Generator().manual_seed(2)).to(torch.bfloat16)
+    sweep = {}
+    clocks = None
+    for drop in c["sweep"]:
+        pol = L.PolicyConfig(mode="latency", drop_count=drop)
+        stack = L.DecodeStack(model, attn, B, max_len=P + args.warmup + args.steps + 4, policy=pol)
+        stack.prefill(x)
+        for _ in range(args.warmup):
+            stack.step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(torch.cuda.current_device()) as cs:
+            e0.record()
+            for _ in range(args.steps):
+                stack.step()
+            e1.record()
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        assert bool(torch.isfinite(stack.prev.float()).all()), "decode stack produced non-finite states"
+        flags = [int(layer.flags.item()) for layer in stack._decode_layers]
+        assert not any(f & 2 for f in flags), "non-finite router logits"
+        used = [layer.used_experts() for layer in stack._decode_layers]
+        sweep[N - drop] = {"ms_per_step": ms, "tokens_per_s": B / (ms * 1e-3), "us_per_layer": ms * 1e3 / nl,
+                           "mean_used_experts": statistics.mean(used),
+                           "step_bytes": sum(used) * SWIGLU_BYTES(c),
+                           "achieved_gbs": sum(used) * SWIGLU_BYTES(c) / (ms * 1e-3) / 1e9}
+        if drop == c["drop"]:
+            clocks = cs.summary()
+            head = stack
+        else:
+            del stack
+        log(f"budget {N - drop}: {ms:.3f} ms/step, used {statistics.mean(used):.2f}")
+    best = sweep[N - c["drop"]]
+    # e2e: the caller's host-side view per step -- the step's input state
+    # host->device (pinned), one graphed step, the step's output device->host
+    h_host = torch.randn((B, d)).to(torch.bfloat16).pin_memory()
+    o_host = torch.empty_like(h_host).pin_memory()
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_e2e = min(args.steps, 20)
+    head.prefill(x)
+    c0.record()
+    for _ in range(n_e2e):
+        head.prev.copy_(h_host, non_blocking=True)
+        o_host.copy_(head.step(), non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    ms_e2e = c0.elapsed_time(c1) / n_e2e
+    peak, peak_src = measured_peaks()
+    return {
+        "metric": METRIC, "value": best["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": best["ms_per_step"], "us_per_step": best["ms_per_step"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: random-init Mixtral-shaped bf16 weights (32 layers, 90 GB), N(0,1) prefill inputs",
+        "config": {"workload": c["workload"], "d_model": d, "d_ff": ff, "experts": N, "top_k": k, "layers": nl,
+                   "global_batch": B, "tokens_per_gpu": B, "policy": f"latency drop {c['drop']} (budget "
+                   f"{N - c['drop']})", "parallelism": "single", "prefill_len": P, "d_head": c["d_head"],
+                   "l2": "inputs > L2: each step streams every layer's used experts (>= 45 GB) >> 126 MB L2",
+                   "budget_sweep": sweep},
+        "roofline": {"bound": "hbm", "kernel": "whole decode step (32 x [attention, K0..K4])",
+                     "achieved": best["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": best["achieved_gbs"] / peak, "peak_source": peak_src,
+                     "frac_of_8TBs": best["achieved_gbs"] / 8000.0, "algorithmic_bytes_per_step": best["step_bytes"],
+                     "traffic": None},
+        "e2e": {"value": B / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": B * d * 2, "d2h_bytes_per_step": B * d * 2,
+                "api": "paper_2411_08982_b200.DecodeStack.step (one CUDA graph per step)"},
+        "gpu_launches": (nl * 7 + 1) * args.steps,
+        "clocks": clocks,
+    }
+
+
 def run_ep(args, c, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -429,10 +519,14 @@ def main():
     ap.add_argument("--impl", choices=["lynx", "reference"], default="lynx")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tokens", type=int, default=None, help="override the config's batch (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.tokens:
+        c["T"] = args.tokens
+        c["workload"] += f"-T{args.tokens}"
     if args.impl == "reference":
         return run_reference(args, c)
 
@@ -446,6 +540,8 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         result = run_ep(args, c, rank, world, local_rank)
+    elif "layers" in c:
+        result = run_stack(args, c)
     else:
         result = run_single(args, c)
     if rank == 0:

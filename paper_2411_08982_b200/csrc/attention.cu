@@ -76,6 +76,13 @@ __device__ __forceinline__ float load_row(const AttnArgs& a, int row, float* x, 
   return scale;
 }
 
+// Latency shaping: the grid spreads a token's work over several CTAs
+// (blockIdx.y) so every lane issues all of its 16-byte weight loads at once
+// and a kernel costs a couple of L2 round trips.  qkv: one projection per
+// warp, 8 per CTA.  out: 1024 output columns per CTA (4 per thread).
+constexpr int kQkvPerCta = kAttnThreads / 32;
+constexpr int kOutCols = kAttnThreads * 4;
+
 __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ float x[];  // [d]
   __shared__ float red[32];
@@ -84,33 +91,37 @@ __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_con
   const int row = blockIdx.x;  // b * Tn + i
   const int b = row / a.Tn, i = row - b * a.Tn;
   const float scale = load_row(a, row, x, red);
-  const int pos = *a.pos + i;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nout = 3 * a.dh;
-  for (int o = warp; o < nout; o += nw) {
-    const uint4* wr = reinterpret_cast<const uint4*>(a.wqkv + static_cast<size_t>(o) * a.d);
-    float acc = 0.f;
-    for (int v = lane; v < (a.d >> 3); v += 32) {
-      const uint4 u = wr[v];
-      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-      const float* xs = x + 8 * v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nout = 3 * a.dh, nvec = a.d >> 3;
+  const int o = blockIdx.y * kQkvPerCta + warp;
+  if (o >= nout) return;
+  const uint4* wr = reinterpret_cast<const uint4*>(a.wqkv + static_cast<size_t>(o) * a.d);
+  float acc = 0.f;
+#pragma unroll 16
+  for (int v = lane; v < nvec; v += 32) {
+    const uint4 u = __ldg(wr + v);
+    const float4 x0 = *reinterpret_cast<const float4*>(x + 8 * v);
+    const float4 x1 = *reinterpret_cast<const float4*>(x + 8 * v + 4);
+    const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float2 f = __bfloat1622float2(w2[0]);
+    acc += x0.x * f.x + x0.y * f.y;
+    f = __bfloat1622float2(w2[1]);
+    acc += x0.z * f.x + x0.w * f.y;
+    f = __bfloat1622float2(w2[2]);
+    acc += x1.x * f.x + x1.y * f.y;
+    f = __bfloat1622float2(w2[3]);
+    acc += x1.z * f.x + x1.w * f.y;
+  }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(w2[j]);
-        acc += xs[2 * j] * f.x + xs[2 * j + 1] * f.y;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kAll, acc, off);
-    if (lane == 0) {
-      acc *= scale;  // (x * s) . w == s * (x . w)
-      const int which = o / a.dh, c = o - which * a.dh;
-      if (which == 0) {
-        a.q[static_cast<size_t>(row) * a.dh + c] = acc;
-      } else {
-        float* cache = which == 1 ? a.kcache : a.vcache;
-        cache[(static_cast<size_t>(b) * a.max_len + pos) * a.dh + c] = acc;
-      }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kAll, acc, off);
+  if (lane == 0) {
+    acc *= scale;  // (x * s) . w == s * (x . w)
+    const int which = o / a.dh, c = o - which * a.dh;
+    if (which == 0) {
+      a.q[static_cast<size_t>(row) * a.dh + c] = acc;
+    } else {
+      float* cache = which == 1 ? a.kcache : a.vcache;
+      cache[(static_cast<size_t>(b) * a.max_len + *a.pos + i) * a.dh + c] = acc;
     }
   }
 }
@@ -118,6 +129,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_con
 __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ float sm[];  // x[d] | scores[max_len] | ctx partials
   __shared__ float red[32];
+  __shared__ float qs[LYNX_MAX_DHEAD];
   __shared__ float ctx[LYNX_MAX_DHEAD];
   griddep_launch_dependents();
   griddep_wait();
@@ -125,19 +137,32 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   const int b = row / a.Tn, i = row - b * a.Tn;
   float* x = sm;
   float* sc = sm + a.d;
-  load_row(a, row, x, red);
+  const int dh = a.dh;
+  if (threadIdx.x < dh) qs[threadIdx.x] = a.q[static_cast<size_t>(row) * dh + threadIdx.x];
+  load_row(a, row, x, red);  // ends with a barrier: qs visible
   const int total = *a.pos + i + 1;  // causal: cache positions 0 .. pos+i
-  const float* q = a.q + static_cast<size_t>(row) * a.dh;
-  const float* K = a.kcache + static_cast<size_t>(b) * a.max_len * a.dh;
-  const float* V = a.vcache + static_cast<size_t>(b) * a.max_len * a.dh;
-  const float inv_sqrt = 1.f / sqrtf(static_cast<float>(a.dh));
+  const float* K = a.kcache + static_cast<size_t>(b) * a.max_len * dh;
+  const float* V = a.vcache + static_cast<size_t>(b) * a.max_len * dh;
+  const float inv_sqrt = 1.f / sqrtf(static_cast<float>(dh));
+  // scores: half a warp per cached position, lanes over the head dimension
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const int hw = (threadIdx.x >> 5) * 2 + half, nhw = (blockDim.x >> 5) * 2;
   float m = -INFINITY;
-  for (int j = threadIdx.x; j < total; j += blockDim.x) {
+  for (int jb = hw - half; jb < total; jb += nhw) {  // warp-uniform trip count
+    const int j = jb + half;
     float s = 0.f;
-    for (int c = 0; c < a.dh; ++c) s += q[c] * K[static_cast<size_t>(j) * a.dh + c];
+    if (j < total) {
+#pragma unroll
+      for (int c0 = 0; c0 < LYNX_MAX_DHEAD; c0 += 16)
+        if (c0 + hl < dh) s += qs[c0 + hl] * K[static_cast<size_t>(j) * dh + c0 + hl];
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(kAll, s, off);
     s *= inv_sqrt;
-    sc[j] = s;
-    m = fmaxf(m, s);
+    if (j < total) {
+      if (hl == 0) sc[j] = s;
+      m = fmaxf(m, s);
+    }
   }
   m = block_max(m, red);
   float l = 0.f;
@@ -147,33 +172,43 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
     l += e;
   }
   l = block_sum(l, red);  // also a barrier: sc[] complete
-  // ctx[c] = sum_j p_j V[j][c]: thread (c, lane-slice of j)
+  // ctx[c] = sum_j p_j V[j][c]: thread (c, slice of j)
   float* part = sc + a.max_len;  // [blockDim/dh][dh]
-  const int per = blockDim.x / a.dh;
-  if (threadIdx.x < per * a.dh) {
-    const int c = threadIdx.x % a.dh, s0 = threadIdx.x / a.dh;
+  const int per = blockDim.x / dh;
+  if (threadIdx.x < per * dh) {
+    const int c = threadIdx.x % dh, s0 = threadIdx.x / dh;
     float acc = 0.f;
-    for (int j = s0; j < total; j += per) acc += sc[j] * V[static_cast<size_t>(j) * a.dh + c];
-    part[s0 * a.dh + c] = acc;
+#pragma unroll 4
+    for (int j = s0; j < total; j += per) acc += sc[j] * V[static_cast<size_t>(j) * dh + c];
+    part[s0 * dh + c] = acc;
   }
   __syncthreads();
-  if (threadIdx.x < a.dh) {
+  if (threadIdx.x < dh) {
     float acc = 0.f;
-    for (int s0 = 0; s0 < per; ++s0) acc += part[s0 * a.dh + threadIdx.x];
+    for (int s0 = 0; s0 < per; ++s0) acc += part[s0 * dh + threadIdx.x];
     ctx[threadIdx.x] = acc / l;
   }
   __syncthreads();
-  // h_out = x + ctx Wo   (Wo stored [dh, d]: coalesced over the columns)
+  // h_out = x + ctx Wo for this CTA's 1024 columns (Wo stored [dh, d]:
+  // coalesced over the columns; every head row's load is in flight at once)
   uint16_t* dst = a.h_out + static_cast<size_t>(row) * a.d;
-  for (int col = threadIdx.x * 2; col < a.d; col += blockDim.x * 2) {
-    float o0 = 0.f, o1 = 0.f;
-    for (int c = 0; c < a.dh; ++c) {
-      const float2 w = __bfloat1622float2(
-          *reinterpret_cast<const __nv_bfloat162*>(a.wo + static_cast<size_t>(c) * a.d + col));
-      o0 += ctx[c] * w.x;
-      o1 += ctx[c] * w.y;
+  const int col = blockIdx.y * kOutCols + threadIdx.x * 4;
+  if (col < a.d) {
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 16
+    for (int c = 0; c < dh; ++c) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(a.wo + static_cast<size_t>(c) * a.d + col));
+      const float2 w0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      o[0] += ctx[c] * w0.x;
+      o[1] += ctx[c] * w0.y;
+      o[2] += ctx[c] * w1.x;
+      o[3] += ctx[c] * w1.y;
     }
-    *reinterpret_cast<__nv_bfloat162*>(dst + col) = __floats2bfloat162_rn(x[col] + o0, x[col + 1] + o1);
+    uint2 out;
+    *reinterpret_cast<__nv_bfloat162*>(&out.x) = __floats2bfloat162_rn(x[col] + o[0], x[col + 1] + o[1]);
+    *reinterpret_cast<__nv_bfloat162*>(&out.y) = __floats2bfloat162_rn(x[col + 2] + o[2], x[col + 3] + o[3]);
+    *reinterpret_cast<uint2*>(dst + col) = out;
   }
 }
 
@@ -199,10 +234,12 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = dev;
   }
-  const dim3 grid(a.B * a.Tn);
-  cudaError_t e = launch_pdl(attn_qkv_kernel, grid, dim3(kAttnThreads), smem_a, s, a);
+  const int rows = a.B * a.Tn;
+  cudaError_t e = launch_pdl(attn_qkv_kernel, dim3(rows, (3 * a.dh + kQkvPerCta - 1) / kQkvPerCta),
+                             dim3(kAttnThreads), smem_a, s, a);
   if (e != cudaSuccess) return e;
-  return launch_pdl(attn_out_kernel, grid, dim3(kAttnThreads), smem_b, s, a);
+  return launch_pdl(attn_out_kernel, dim3(rows, (a.d + kOutCols - 1) / kOutCols), dim3(kAttnThreads), smem_b, s,
+                    a);
 }
 
 cudaError_t launch_advance_position(int32_t* pos, int by, cudaStream_t s) {

@@ -100,11 +100,14 @@ class MoEWeights:
         return 3 * s.d_model * s.d_ff * 2 if self.activation == "swiglu" else 2 * s.d_model * s.d_ff * 2
 
 
-def build_swiglu_model(spec: MoEModelSpec, seed: int = 0, router_gain: float = 2.0,
+def build_swiglu_model(spec: MoEModelSpec, seed: int = 0, router_gain: float = 2.0, expert_gain: float = 1.0,
                        device: str = "cuda") -> MoEWeights:
     """Random-init SwiGLU stack (SURVEY 8d recipe, after simulator.py:44-74):
-    router ~ N(0, (gain/sqrt(d))^2), W1, W3 ~ N(0, 1/d), W2 ~ N(0, 1/ff); bf16.
-    Shared experts (spec.num_shared_experts) are experts N..N+S-1 of w13/w2."""
+    router ~ N(0, (gain/sqrt(d))^2), W1, W3 ~ N(0, 1/d), W2 ~ N(0, (expert_gain *
+    out_damp / sqrt(ff))^2) with the reference's depth damping out_damp =
+    1/sqrt(2L) (simulator.py:64-73), so a deep stack keeps bounded hidden
+    norms; bf16.  Shared experts (spec.num_shared_experts) are experts
+    N..N+S-1 of w13/w2."""
     torch = _torch()
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -120,7 +123,7 @@ def build_swiglu_model(spec: MoEModelSpec, seed: int = 0, router_gain: float = 2
                 rows = 128 * (f // 64) + 32 * ((f % 64) // 16) + (16 if up else 0) + f % 16
                 w13[:, rows.to(device)] = 0
         w2 = torch.randn((E, d, ff), generator=g, device=device, dtype=torch.bfloat16)
-        w2.mul_(1.0 / np.sqrt(ff))
+        w2.mul_(expert_gain / np.sqrt(2.0 * spec.num_layers) / np.sqrt(ff))
         r = torch.randn((N, d), generator=g, device=device, dtype=torch.bfloat16)
         r.mul_(router_gain / np.sqrt(d))
         w13s.append(w13)
