@@ -251,6 +251,35 @@ class DecodeStack:
         self.steps_done += 1
         return self.prev
 
+    def profile_step(self) -> dict:
+        """One eager decode step with CUDA events around every kernel group;
+        returns milliseconds per step split the way the reference's cost
+        model calibration table is (costmodel.py:300-343): attention,
+        routing (router GEMV + selection), MLP (gather + expert FFN +
+        combine).  Event records serialise the programmatic launches, so
+        the parts sum to slightly more than a graphed step."""
+        torch = _torch()
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        marks = []
+        h = self.prev
+        for l in range(self.L):
+            a0, a1 = ev(), ev()
+            k = [ev() for _ in range(6)]
+            a0.record()
+            self._attention(l, h, 1, l == 0, self._mid, self._attn_ws)
+            a1.record()
+            dst = self.prev if l == self.L - 1 else self._alt[l % 2]
+            self._decode_layers[l].profiled(self._mid, k, dst)
+            marks.append((a0, a1, k))
+            h = dst
+        self._advance(1)
+        torch.cuda.synchronize()
+        attn = sum(a0.elapsed_time(a1) for a0, a1, _ in marks)
+        route = sum(k[0].elapsed_time(k[2]) for _, _, k in marks)
+        mlp = sum(k[2].elapsed_time(k[5]) for _, _, k in marks)
+        self.steps_done += 1
+        return {"attn_ms": attn, "route_ms": route, "mlp_ms": mlp}
+
     def simulate(self, inputs, decode_steps: int) -> SimResult:
         """simulator.py:273-357 for one batch: prefill then decode_steps greedy steps."""
         torch = _torch()
