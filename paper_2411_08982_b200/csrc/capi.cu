@@ -115,7 +115,8 @@ Geometry geometry(const lynx_layer_t* L, int T) {
 // Workspace carve-up.  Selection region only for the whole-layer call.
 struct Plan {
   size_t logits, ids, probs, full, conf, counts, retained, assigned, weights, important, flags;
-  size_t n_seg, n_used, n_rows, seg_expert, seg_row, seg_count, perm_token, perm_weight, tok_rows, tok_weight;
+  size_t n_seg, n_used, n_rows, seg_expert, seg_row, seg_count, seg_order, perm_token, perm_weight, tok_rows,
+      tok_weight;
   size_t counters, x_perm, h, y;
   size_t total;
   int n_counters;
@@ -151,6 +152,7 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.seg_expert = take(sizeof(int32_t) * c.max_seg);
   p.seg_row = take(sizeof(int32_t) * c.max_seg);
   p.seg_count = take(sizeof(int32_t) * c.max_seg);
+  p.seg_order = take(sizeof(int32_t) * c.max_seg);
   p.perm_token = take(sizeof(int32_t) * c.rows_cap);
   p.perm_weight = take(sizeof(float) * c.rows_cap);
   p.tok_rows = take(sizeof(int32_t) * T * (k + S));
@@ -219,6 +221,7 @@ PlanOut plan_out(void* ws, const Plan& P, int n_shared) {
   o.seg_expert = at<int32_t>(ws, P.seg_expert);
   o.seg_row = at<int32_t>(ws, P.seg_row);
   o.seg_count = at<int32_t>(ws, P.seg_count);
+  o.seg_order = at<int32_t>(ws, P.seg_order);
   o.perm_token = at<int32_t>(ws, P.perm_token);
   o.perm_weight = at<float>(ws, P.perm_weight);
   o.tok_rows = at<int32_t>(ws, P.tok_rows);
@@ -271,6 +274,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.seg_expert = o.seg_expert;
   fp.seg_row = o.seg_row;
   fp.seg_count = o.seg_count;
+  fp.seg_order = o.seg_order;
   fp.h = at<uint16_t>(ws, P.h);
   fp.partial = at<float>(ws, P.y);
   fp.counters = o.counters;
@@ -530,6 +534,7 @@ int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t*
   o.seg_expert = out->seg_expert;
   o.seg_row = out->seg_row;
   o.seg_count = out->seg_count;
+  o.seg_order = nullptr;
   o.perm_token = out->perm_token;
   o.perm_weight = out->perm_weight;
   o.tok_rows = out->tok_rows;

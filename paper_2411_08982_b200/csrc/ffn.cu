@@ -57,10 +57,11 @@ struct Unit {
 __device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u, Unit& U) {
   if (u < 0) return false;
   const int nA = nseg * p.tiles1;
+  int slot;
   if (u < nA) {
     U.phase = 0;
-    U.seg = u / p.tiles1;
-    U.mt = u - U.seg * p.tiles1;
+    slot = u / p.tiles1;
+    U.mt = u - slot * p.tiles1;
     U.split = 0;
     U.kb0 = 0;
     U.kb1 = p.kb1;
@@ -68,13 +69,17 @@ __device__ __forceinline__ bool decode_unit(const FfnParams& p, int nseg, int u,
     const int v = u - nA;
     const int per = p.tiles2 * p.split2;
     U.phase = 1;
-    U.seg = v / per;
-    const int r = v - U.seg * per;
+    slot = v / per;
+    const int r = v - slot * per;
     U.mt = r / p.split2;
     U.split = r - U.mt * p.split2;
     U.kb0 = U.split * p.kb2_per;
     U.kb1 = min(p.kb2_total, U.kb0 + p.kb2_per);
   }
+  // queue slots run the largest segments first (LPT), so the last units of
+  // the launch -- and the phase-1 units waiting on the last phase-0 tiles --
+  // are the cheapest ones
+  U.seg = p.seg_order[slot];
   U.expert = p.seg_expert[U.seg];
   U.row0 = p.seg_row[U.seg];
   U.n = p.seg_count[U.seg];

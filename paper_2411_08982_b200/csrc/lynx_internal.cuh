@@ -53,6 +53,7 @@ struct PlanOut {
   int32_t* seg_expert;
   int32_t* seg_row;
   int32_t* seg_count;
+  int32_t* seg_order;   // [max_seg] K3 queue order: segments by rows desc (LPT), or null
   int32_t* perm_token;  // [rows_cap] source token, -1 = padding
   float* perm_weight;
   int32_t* tok_rows;    // [T,k+S] permuted rows per token: routed experts ascending (-1 padded),
@@ -91,6 +92,7 @@ struct FfnParams {
   const int32_t* seg_expert;
   const int32_t* seg_row;
   const int32_t* seg_count;
+  const int32_t* seg_order;  // queue slot -> segment (largest first)
   uint16_t* h;      // [rows_cap, ff] bf16
   float* partial;   // [split2, rows_cap, d] f32
   int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s

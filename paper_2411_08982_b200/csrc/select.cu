@@ -33,6 +33,23 @@ namespace lynx {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Diagnostic library only (-DLYNX_TRACE): phase timestamps of the last K1.
+#ifdef LYNX_TRACE
+__device__ unsigned long long g_sel_ts[32];
+#define SEL_TS(i)                                      \
+  do {                                                 \
+    __syncthreads();                                   \
+    if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
+  } while (0)
+#define SEL_TS_LOCAL(i) \
+  do {                                                 \
+    if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
+  } while (0)
+#else
+#define SEL_TS(i) (void)0
+#define SEL_TS_LOCAL(i) (void)0
+#endif
+
 // numpy's pairwise float64 summation (oracle.pairwise_sum): < 8 terms added
 // left to right; <= 128 terms with 8 strided partials folded pairwise plus
 // the tail; longer runs split at an 8-aligned midpoint.
@@ -212,6 +229,8 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
   __shared__ int s_cnt[LYNX_MAX_EXPERTS];
   __shared__ int s_base[LYNX_MAX_EXPERTS];
   __shared__ int s_shared_base;
+  constexpr int kOrderMax = 256;  // segments ranked in shared memory (more: identity order)
+  __shared__ int s_segcnt[kOrderMax];
   const int W = (T + 31) >> 5;
   const int S = o.n_shared, kk = k + S, T16 = (T + 15) & ~15;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -275,9 +294,11 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
       if (e < N) s_base[e] = base[h];
       #pragma unroll 1
       for (int c = 0; c < nsg[h]; ++c) {
+        const int rows = min(LYNX_SEG_ROWS, cnt[h] - c * LYNX_SEG_ROWS);
         o.seg_expert[seg[h] + c] = e;
         o.seg_row[seg[h] + c] = base[h] + c * LYNX_SEG_ROWS;
-        o.seg_count[seg[h] + c] = min(LYNX_SEG_ROWS, cnt[h] - c * LYNX_SEG_ROWS);
+        o.seg_count[seg[h] + c] = rows;
+        if (seg[h] + c < kOrderMax) s_segcnt[seg[h] + c] = rows;
       }
     }
     const int nused = __popc(__ballot_sync(kFull, cnt[0] > 0)) + __popc(__ballot_sync(kFull, cnt[1] > 0));
@@ -286,9 +307,11 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     #pragma unroll 1
     for (int i = lane; i < S * seg_per_shared; i += 32) {
       const int sx = i / seg_per_shared, c = i - sx * seg_per_shared;
+      const int rows = min(LYNX_SEG_ROWS, T - c * LYNX_SEG_ROWS);
       o.seg_expert[seg_off + i] = N + sx;
       o.seg_row[seg_off + i] = row_off + sx * T16 + c * LYNX_SEG_ROWS;
-      o.seg_count[seg_off + i] = min(LYNX_SEG_ROWS, T - c * LYNX_SEG_ROWS);
+      o.seg_count[seg_off + i] = rows;
+      if (seg_off + i < kOrderMax) s_segcnt[seg_off + i] = rows;
     }
     if (lane == 0) {
       s_shared_base = row_off;
@@ -298,6 +321,24 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     }
   }
   __syncthreads();
+  if (o.seg_order) {  // K3 queue order: rows desc, segment index asc (largest first)
+    const int nseg = *o.n_seg;  // written by lane 0 above; visible after the barrier
+    #pragma unroll 1
+    for (int i = tid; i < nseg; i += nthr) {
+      if (nseg > kOrderMax) {
+        o.seg_order[i] = i;
+        continue;
+      }
+      const int ci = s_segcnt[i];
+      int rank = 0;
+      #pragma unroll 4
+      for (int j = 0; j < nseg; ++j) {
+        const int cj = s_segcnt[j];
+        rank += (cj > ci || (cj == ci && j < i)) ? 1 : 0;
+      }
+      o.seg_order[rank] = i;
+    }
+  }
   // Per token: its distinct experts ascending (bit scan of a 64-bit set), the
   // permuted row of each and the merged weight 0 + sum of its slots on that
   // expert in slot order (simulator.py:108-111).
@@ -408,6 +449,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     }
     if (local) atomicAdd(s_nq, local);
     __syncthreads();
+    SEL_TS_LOCAL(16);
     const int nq = *s_nq;
     const int S = a.pol.sample_threshold;
     if (nq == 0) {
@@ -439,6 +481,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     }
     __syncthreads();
   }
+  SEL_TS_LOCAL(17);
   // Unit votes are integers: order-free atomics are exact.  Rank-weighted
   // votes are float sums and keep numpy's slot order (thread per expert).
   if (!a.pol.n_rank_weights) {
@@ -463,6 +506,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     }
   }
   __syncthreads();
+  SEL_TS_LOCAL(18);
   #pragma unroll 1
   for (int e = tid; e < N; e += nthr) {  // retention order: count desc, index asc
     const double ce = s_counts[e];
@@ -476,6 +520,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     s_order[rank] = e;
   }
   __syncthreads();
+  SEL_TS_LOCAL(19);
   if (!accuracy) {  // latency_policy
     const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
     const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
@@ -510,22 +555,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   }
 }
 
-// Diagnostic library only (-DLYNX_TRACE): phase timestamps of the last K1.
-#ifdef LYNX_TRACE
-__device__ unsigned long long g_sel_ts[16];
-#define SEL_TS(i)                                      \
-  do {                                                 \
-    __syncthreads();                                   \
-    if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
-  } while (0)
-#define SEL_TS_LOCAL(i) \
-  do {                                                 \
-    if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
-  } while (0)
-#else
-#define SEL_TS(i) (void)0
-#define SEL_TS_LOCAL(i) (void)0
-#endif
+
 
 // ------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(const __grid_constant__ SelectArgs a) {
@@ -1401,6 +1431,6 @@ cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_poli
 
 #ifdef LYNX_TRACE
 extern "C" int lynx_debug_select_ts(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, lynx::g_sel_ts, sizeof(lynx::g_sel_ts)) == cudaSuccess ? 16 : -1;
+  return cudaMemcpyFromSymbol(host, lynx::g_sel_ts, sizeof(lynx::g_sel_ts)) == cudaSuccess ? 32 : -1;
 }
 #endif

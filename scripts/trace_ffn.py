@@ -27,10 +27,15 @@ def main():
     lib = nat.lib()
     lib.lynx_debug_trace.restype = ctypes.c_int
     lib.lynx_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    T, N, k, d, ff = 32, 8, 2, 4096, 14336
-    spec = L.MoEModelSpec(1, N, k, d, ff)
+    if "--c4" in sys.argv:
+        T, N, k, d, ff, S = 128, 64, 6, 2048, 1408, 2
+        pol = L.PolicyConfig(mode="accuracy", freq_keep_budget=16)
+    else:
+        T, N, k, d, ff, S = 32, 8, 2, 4096, 14336, 0
+        pol = L.PolicyConfig(mode="latency", drop_count=4)
+    spec = L.MoEModelSpec(1, N, k, d, ff, num_shared_experts=S)
     model = L.build_swiglu_model(spec, seed=0)
-    layer = L.LynxMoELayer(model, 0, T, policy=L.PolicyConfig(mode="latency", drop_count=4))
+    layer = L.LynxMoELayer(model, 0, T, policy=pol)
     h = torch.randn((T, d), device="cuda").to(torch.bfloat16)
     for _ in range(3):
         layer(h)
@@ -49,6 +54,7 @@ def main():
     base = t0.min()
     used = layer.used_experts()
     nrows = int(((torch.bincount(layer.assigned.flatten().long(), minlength=N) + 15) // 16 * 16).sum().item())
+    nseg = int(layer.workspace.new_tensor([0]).numel())  # placeholder (segments = used experts here)
     # unit classes (queue order: gather rows, phase-0, phase-1)
     tiles1 = 2 * ((ff + 63) // 64) * 64 // 128
     ngather = nrows if os.environ.get("LYNX_FUSED_GATHER", "0") == "1" else 0

@@ -40,10 +40,14 @@ def main():
                 for _ in range(2):
                     sel = L.route_batch(L.RoutingLogits(0, L.Phase.DECODE, lg), k, check=False)
                     torch.cuda.synchronize()
-            buf = np.zeros(16, dtype=np.uint64)
+            buf = np.zeros(32, dtype=np.uint64)
             lib.lynx_debug_select_ts(buf.ctypes.data)
             ts = buf[:7].astype(np.int64)
             rows.append(np.diff(ts) / 1e3)
+            if buf[16]:  # policy sub-phases (thread 0): important, ranking, votes, retention order, keep
+                sub = buf[[2, 16, 17, 18, 19, 3]].astype(np.int64)
+                print(label, "policy sub-phases (us): important, sample-rank, votes, order, keep:",
+                      np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
             if buf[8]:  # group path sub-phases (warp 0's own timeline)
                 sub = buf[[1, 8, 9, 10, 11, 12, 13]].astype(np.int64)
                 print(label, "route sub-phases (us): load+max, exp, sum, div, write, topk:",
