@@ -437,6 +437,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
                                           int* s_keep, double* s_counts, int* s_icount, int* s_rank, int* s_order,
                                           int* s_nq, int* s_clipped) {
   const int T = a.T, N = a.N, k = a.k, tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
   const bool accuracy = a.pol.mode == LYNX_POLICY_ACCURACY;
   if (accuracy) {  // select_important_tokens
     const double tau = a.pol.confidence_threshold;
@@ -453,27 +454,42 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     const int nq = *s_nq;
     const int S = a.pol.sample_threshold;
     if (nq == 0) {
-      if (tid == 0) {
-        int best = 0;
+      if (warp == 0) {  // [argmax conf]: first maximum, one warp
+        double best = -1.0;
+        int bi = -1;
         #pragma unroll 1
-        for (int t = 1; t < T; ++t)
-          if (CONF[t] > CONF[best]) best = t;
-        IMP[best] = 1;
+        for (int t = lane; t < T; t += 32)
+          if (bi < 0 || CONF[t] > best) {
+            best = CONF[t];
+            bi = t;
+          }
+        #pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ob = __shfl_xor_sync(kFull, best, off);
+          const int oi = __shfl_xor_sync(kFull, bi, off);
+          if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) IMP[bi] = 1;
       }
     } else if (nq > S) {
-      // keep the S most confident (conf desc, t asc); ranks read CONF only,
-      // so marking drops in bit 1 is race-free
+      // keep the S most confident (conf desc, t asc): a warp per candidate,
+      // lanes count the better candidates; ranks read CONF only, so marking
+      // drops in bit 1 is race-free
       #pragma unroll 1
-      for (int t = tid; t < T; t += nthr) {
-        if (!IMP[t]) continue;
+      for (int t = warp; t < T; t += nwarps) {
+        if (!IMP[t]) continue;  // warp-uniform
         const double ct = CONF[t];
-        int rank = 0;
+        int better = 0;
         #pragma unroll 1
-        for (int u = 0; u < T; ++u) {
+        for (int u = lane; u < T; u += 32) {
           const double cu = CONF[u];
-          rank += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
+          better += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
         }
-        if (rank >= S) IMP[t] |= 2;
+        better = __reduce_add_sync(kFull, better);
+        if (lane == 0 && better >= S) IMP[t] |= 2;
       }
       __syncthreads();
       #pragma unroll 1
@@ -507,17 +523,37 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   }
   __syncthreads();
   SEL_TS_LOCAL(18);
+  // retention order (count desc, index asc): a thread per expert for small
+  // N, else a warp per expert with one ballot per 32 competitors
+  if (N <= 32 || nwarps < 4) {
+    #pragma unroll 1
+    for (int e = tid; e < N; e += nthr) {
+      const double ce = s_counts[e];
+      int rank = 0;
+      #pragma unroll 4
+      for (int f = 0; f < N; ++f) {
+        const double cf = s_counts[f];
+        rank += (cf > ce || (cf == ce && f < e)) ? 1 : 0;
+      }
+      s_rank[e] = rank;
+      s_order[rank] = e;
+    }
+  } else {
   #pragma unroll 1
-  for (int e = tid; e < N; e += nthr) {  // retention order: count desc, index asc
+  for (int e = warp; e < N; e += nwarps) {
     const double ce = s_counts[e];
     int rank = 0;
     #pragma unroll 1
-    for (int f = 0; f < N; ++f) {
-      const double cf = s_counts[f];
-      rank += (cf > ce || (cf == ce && f < e)) ? 1 : 0;
+    for (int f0 = 0; f0 < N; f0 += 32) {
+      const int f = f0 + lane;
+      const double cf = f < N ? s_counts[f] : 0.0;
+      rank += __popc(__ballot_sync(kFull, f < N && (cf > ce || (cf == ce && f < e))));
     }
-    s_rank[e] = rank;
-    s_order[rank] = e;
+    if (lane == 0) {
+      s_rank[e] = rank;
+      s_order[rank] = e;
+    }
+  }
   }
   __syncthreads();
   SEL_TS_LOCAL(19);
@@ -536,26 +572,24 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
     for (int t = tid; t < T; t += nthr)
       if (IMP[t]) s_keep[IDS[t * k]] = 1;
     __syncthreads();
-    if (tid == 0) {
-      int cnt = 0;
-      #pragma unroll 1
-      for (int e = 0; e < N; ++e) cnt += s_keep[e];
-      int padded = 0;
-      #pragma unroll 1
-      for (int pos = 0; pos < N && cnt < a.floor_keep; ++pos) {
-        const int e = s_order[pos];
-        if (!s_keep[e]) {
-          s_keep[e] = 1;
-          ++cnt;
-          padded = 1;
-        }
+    if (warp == 0) {
+      // pad from the retention order up to the floor: the first (floor - kept)
+      // unkept experts by rank, found with two ballots (N <= 64)
+      const bool k0 = lane < N && s_keep[lane], k1 = lane + 32 < N && s_keep[lane + 32];
+      const int kept = __popc(__ballot_sync(kFull, k0)) + __popc(__ballot_sync(kFull, k1));
+      const int need = a.floor_keep - kept;
+      if (need > 0) {
+        const int e0 = lane < N ? s_order[lane] : -1, e1 = lane + 32 < N ? s_order[lane + 32] : -1;
+        const bool u0 = e0 >= 0 && !s_keep[e0], u1 = e1 >= 0 && !s_keep[e1];
+        const unsigned b0 = __ballot_sync(kFull, u0), b1 = __ballot_sync(kFull, u1);
+        const unsigned below = (1u << lane) - 1u;
+        if (u0 && __popc(b0 & below) < need) s_keep[e0] = 1;
+        if (u1 && __popc(b0) + __popc(b1 & below) < need) s_keep[e1] = 1;
       }
-      *s_clipped = padded;
+      if (lane == 0) *s_clipped = need > 0;
     }
   }
 }
-
-
 
 // ------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(kSelectThreads) route_select_kernel(const __grid_constant__ SelectArgs a) {
@@ -938,32 +972,55 @@ __device__ __forceinline__ double grp_pairwise(const double (&v)[EPL], int n, in
   return r;
 }
 
-// best expert of `cand` by (value desc, index asc) over a group row; -1 if
-// none.  (Comparing the doubles' bit patterns as 64-bit integers instead was
-// measured 30% slower: 64-bit integer compares are multi-instruction.)
+// Lane-local candidate masks: bit m of lane j's mask <-> expert j + 8m.
 template <int EPL>
-__device__ __forceinline__ int grp_best(const double (&v)[EPL], uint64_t cand, int j, double* bv) {
-  int bi = -1;
-  double best = 0.0;
+__device__ __forceinline__ uint32_t lane_bits(uint64_t mask, int j) {
+  uint32_t l = 0;
+#pragma unroll
+  for (int m = 0; m < EPL; ++m) l |= static_cast<uint32_t>((mask >> (j + 8 * m)) & 1ull) << m;
+  return l;
+}
+
+__device__ __forceinline__ void lane_mark(uint32_t& l, int e, int j) {
+  if ((e & 7) == j) l |= 1u << (e >> 3);
+}
+
+// best expert among the lane-local candidates by (value desc, index asc); -1
+// if none.  In-lane: a depth-log2(EPL) tree over adjacent ranges (the lower
+// slot of a pair covers the lower ids, so strict > keeps ties on the smaller
+// id); across the group:
+// three xor-shuffles.  "None" is (-1.0, 64): probabilities are >= 0.
+template <int EPL>
+__device__ __forceinline__ int grp_best(const double (&v)[EPL], uint32_t cand, int j, double* bv) {
+  double bvv[EPL];
+  int bm[EPL];
 #pragma unroll
   for (int m = 0; m < EPL; ++m) {
-    const int e = j + 8 * m;
-    if (((cand >> e) & 1ull) && (bi < 0 || v[m] > best)) {  // ascending e: ties keep the smaller
-      bi = e;
-      best = v[m];
-    }
+    const bool c = (cand >> m) & 1u;
+    bvv[m] = c ? v[m] : -1.0;
+    bm[m] = c ? j + 8 * m : 64;
   }
+#pragma unroll
+  for (int st = 1; st < EPL; st <<= 1)  // adjacent ranges: slot m always holds the lower ids
+#pragma unroll
+    for (int m = 0; m + st < EPL; m += 2 * st)
+      if (bvv[m + st] > bvv[m]) {
+        bvv[m] = bvv[m + st];
+        bm[m] = bm[m + st];
+      }
+  double best = bvv[0];
+  int bi = bm[0];
 #pragma unroll
   for (int off = 1; off < kGroup; off <<= 1) {
     const double ov = __shfl_xor_sync(kFull, best, off);
     const int oi = __shfl_xor_sync(kFull, bi, off);
-    if (oi >= 0 && (bi < 0 || ov > best || (ov == best && oi < bi))) {
+    if (ov > best || (ov == best && oi < bi)) {
       best = ov;
       bi = oi;
     }
   }
   *bv = best;
-  return bi;
+  return bi == 64 ? -1 : bi;
 }
 
 template <int EPL>
@@ -989,7 +1046,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   int32_t* ASG = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.asg) : a.assigned;
   double* WT = a.stage ? reinterpret_cast<double*>(s_dyn + L.w) : a.weights;
   uint8_t* IMP = s_dyn + L.imp;
-  const uint64_t all = expert_mask_all(N);
+  const uint32_t all_l = lane_bits<EPL>(expert_mask_all(N), j);
   if (tid == 0) {
     s_flags = 0;
     s_nq = 0;
@@ -1040,12 +1097,12 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
           }
       }
       SEL_TS_LOCAL(12);
-      uint64_t taken = 0;
+      uint32_t taken = ~all_l;
 #pragma unroll 1
       for (int r = 0; r < k; ++r) {
         double bv;
-        const int b = grp_best<EPL>(v, all & ~taken, j, &bv);
-        taken |= 1ull << b;
+        const int b = grp_best<EPL>(v, ~taken, j, &bv);
+        lane_mark(taken, b, j);
         if (live && j == 0) {
           IDS[t * k + r] = b;
           PROBS[t * k + r] = bv;
@@ -1069,14 +1126,16 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
     }
     SEL_TS_LOCAL(13);
     double top1;
-    const int first = grp_best<EPL>(v, all, j, &top1);
+    const int first = grp_best<EPL>(v, all_l, j, &top1);
     double c = top1;
     if (a.pol.confidence_metric == LYNX_CONF_MARGIN) {
       if (N == 1) {
         c = grp_at<EPL>(v, 0, gbase);
       } else {
         double second;
-        grp_best<EPL>(v, all & ~(1ull << first), j, &second);
+        uint32_t rest = all_l;
+        if ((first & 7) == j) rest &= ~(1u << (first >> 3));
+        grp_best<EPL>(v, rest, j, &second);
         c = top1 - second;
       }
     }
@@ -1108,61 +1167,66 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   // 2) remap onto the retained set (policy.py:171-210), or the identity
   // mask with weights = probs / row sum (policy.py:215-229)
   const uint64_t keep = s_keepmask;
+  const uint32_t keep_l = lane_bits<EPL>(keep, j);
+  SEL_TS_LOCAL(20);
 #pragma unroll 1
   for (int t = grp; t < Tw; t += ngrp) {
     const bool live = t < T;
-    double slot[LYNX_MAX_TOPK];
-    int asg[LYNX_MAX_TOPK];
     if (run_policy) {
+      // rolled slot loop (one inlined arg-max): the kernel runs from a cold
+      // instruction cache once per layer, so code size is latency.  Slot
+      // probabilities park in WT until the row's renormalisation.
       double v[EPL];
 #pragma unroll
       for (int q = 0; q < EPL; ++q) {
         const int e = j + 8 * q;
         v[q] = (live && e < N) ? P[static_cast<size_t>(t) * N + e] : 0.0;
       }
-      int ids[LYNX_MAX_TOPK];
-      uint64_t occupied = 0;
-#pragma unroll
-      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
-        ids[r] = (live && r < k) ? IDS[t * k + r] : 0;
-        if (r < k && ((keep >> ids[r]) & 1ull)) occupied |= 1ull << ids[r];
+      uint32_t occ = 0;  // lane-local: retained original choices
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+        const int e = live ? IDS[t * k + r] : 0;
+        if ((keep >> e) & 1ull) lane_mark(occ, e, j);
       }
-#pragma unroll
-      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
-        slot[r] = 0.0;
-        asg[r] = 0;
-        if (r < k) {  // shuffles stay warp-uniform: every group runs the arg-max
-          int e = ids[r];
-          double bv;
-          int pick = grp_best<EPL>(v, keep & ~occupied, j, &bv);
-          if (__any_sync(kFull, pick < 0)) {
-            const int any = grp_best<EPL>(v, keep, j, &bv);  // collapse (policy.py:197-200)
-            if (pick < 0) pick = any;
-          }
-          if (!((keep >> e) & 1ull)) {
-            e = pick;
-            occupied |= 1ull << e;
-          }
-          asg[r] = e;
-          slot[r] = grp_at<EPL>(v, e, gbase);
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {  // shuffles stay warp-uniform: every group runs the arg-max
+        int e = live ? IDS[t * k + r] : 0;
+        double bv;
+        int pick = grp_best<EPL>(v, keep_l & ~occ, j, &bv);
+        if (__any_sync(kFull, pick < 0)) {
+          const int any = grp_best<EPL>(v, keep_l, j, &bv);  // collapse (policy.py:197-200)
+          if (pick < 0) pick = any;
         }
+        if (!((keep >> e) & 1ull)) {
+          e = pick;
+          lane_mark(occ, e, j);
+        }
+        const double val = grp_at<EPL>(v, e, gbase);
+        if (live && j == 0) {
+          ASG[t * k + r] = e;
+          WT[t * k + r] = val;
+        }
+        if (r == 0) SEL_TS_LOCAL(21);
       }
-    } else {
-#pragma unroll
-      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
-        asg[r] = (live && r < k) ? IDS[t * k + r] : 0;
-        slot[r] = (live && r < k) ? PROBS[t * k + r] : 0.0;
+      SEL_TS_LOCAL(22);
+    } else if (live && j == 0) {
+#pragma unroll 1
+      for (int r = 0; r < k; ++r) {
+        ASG[t * k + r] = IDS[t * k + r];
+        WT[t * k + r] = PROBS[t * k + r];
       }
     }
+    __syncwarp();
+    SEL_TS_LOCAL(23);
     if (live && j == 0) {
+      double slot[LYNX_MAX_TOPK];
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r) slot[r] = r < k ? WT[t * k + r] : 0.0;
       const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot, k);
       if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);
 #pragma unroll
       for (int r = 0; r < LYNX_MAX_TOPK; ++r)
-        if (r < k) {
-          ASG[t * k + r] = asg[r];
-          WT[t * k + r] = slot[r] / total;
-        }
+        if (r < k) WT[t * k + r] = slot[r] / total;
     }
   }
   __syncthreads();

@@ -48,6 +48,10 @@ def main():
                 sub = buf[[2, 16, 17, 18, 19, 3]].astype(np.int64)
                 print(label, "policy sub-phases (us): important, sample-rank, votes, order, keep:",
                       np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
+            if buf[20]:  # group remap sub-phases (thread 0)
+                sub = buf[[3, 20, 21, 22, 23, 4]].astype(np.int64)
+                print(label, "remap sub-phases (us): start, slot0, slots1.., pre-sum, sum+write:",
+                      np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
             if buf[8]:  # group path sub-phases (warp 0's own timeline)
                 sub = buf[[1, 8, 9, 10, 11, 12, 13]].astype(np.int64)
                 print(label, "route sub-phases (us): load+max, exp, sum, div, write, topk:",
