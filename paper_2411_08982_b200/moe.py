@@ -331,6 +331,67 @@ class LynxMoELayer:
         graphs[key][0].replay()
         return out_host
 
+    def stream_host(self, hidden_hosts, out_hosts):
+        """Run the layer over a sequence of PINNED HOST batches with the PCIe
+        copies overlapped: while the layer (one graph replay) computes batch
+        i, a copy stream moves batch i+1 host->device and batch i-1's output
+        device->host.  Double-buffered device slots; every batch's own H2D and
+        D2H still happens, they just hide behind the neighbouring batches'
+        expert streams.  Results land in ``out_hosts``; the current stream
+        is ordered after the last copy on return (no host sync)."""
+        torch = _torch()
+        n = len(hidden_hosts)
+        if n != len(out_hosts):
+            raise ValidationError("stream_host needs one output buffer per input batch")
+        d = self.model.spec.d_model
+        for t in list(hidden_hosts) + list(out_hosts):
+            if t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != (self.T, d) or not t.is_pinned():
+                raise ValidationError(f"stream_host takes pinned host bf16 tensors of shape [{self.T}, {d}]")
+        st = self.__dict__.get("_stream_state")
+        if st is None:
+            dev_in = [torch.empty((self.T, d), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+            dev_out = [torch.empty_like(dev_in[0]) for _ in range(2)]
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for s_ in range(2):
+                    self(dev_in[s_], dev_out[s_])  # warm-up outside capture
+            torch.cuda.current_stream().wait_stream(side)
+            graphs = []
+            for s_ in range(2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self(dev_in[s_], dev_out[s_])
+                graphs.append(g)
+            st = dict(dev_in=dev_in, dev_out=dev_out, graphs=graphs, copy=torch.cuda.Stream())
+            self._stream_state = st
+        cs, xs = torch.cuda.current_stream(), st["copy"]
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        in_ready, computed, out_copied = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+        xs.wait_stream(cs)
+        with torch.cuda.stream(xs):
+            st["dev_in"][0].copy_(hidden_hosts[0], non_blocking=True)
+            in_ready[0].record(xs)
+        for i in range(n):
+            s_ = i % 2
+            if i + 1 < n:  # next input into the other slot once batch i-1 is done reading it
+                with torch.cuda.stream(xs):
+                    if i >= 1:
+                        xs.wait_event(computed[1 - s_])
+                    st["dev_in"][1 - s_].copy_(hidden_hosts[i + 1], non_blocking=True)
+                    in_ready[1 - s_].record(xs)
+            cs.wait_event(in_ready[s_])
+            if i >= 2:
+                cs.wait_event(out_copied[s_])  # batch i-2's output has left this slot
+            st["graphs"][s_].replay()
+            computed[s_].record(cs)
+            with torch.cuda.stream(xs):
+                xs.wait_event(computed[s_])
+                out_hosts[i].copy_(st["dev_out"][s_], non_blocking=True)
+                out_copied[s_].record(xs)
+        cs.wait_stream(xs)
+        return out_hosts
+
     def profiled(self, hidden, events, out=None):
         """__call__ that records 6 torch.cuda.Events around K0..K4 (lynx_moe_layer_profiled)."""
         torch = _torch()

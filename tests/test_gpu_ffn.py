@@ -237,3 +237,17 @@ def test_host_step_graph_matches_device_call():
         torch.cuda.synchronize()
         ref = layer(h_host.cuda()).cpu()
         assert torch.equal(o_host, ref), step
+
+
+def test_stream_host_matches_device_calls():
+    """LynxMoELayer.stream_host (copy-overlapped host batches) returns exactly
+    the device-resident outputs, batch by batch, including the slot reuse."""
+    spec = L.MoEModelSpec(1, 8, 2, 256, 512)
+    model = L.build_swiglu_model(spec, seed=3)
+    layer = L.LynxMoELayer(model, 0, 16, policy=L.PolicyConfig(mode="latency", drop_count=2))
+    hs = [torch.randn((16, 256)).to(torch.bfloat16).pin_memory() for _ in range(5)]
+    outs = [torch.empty_like(hs[0]).pin_memory() for _ in range(5)]
+    layer.stream_host(hs, outs)
+    torch.cuda.synchronize()
+    for h, o in zip(hs, outs):
+        assert torch.equal(o, layer(h.cuda()).cpu())
