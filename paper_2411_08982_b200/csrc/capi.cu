@@ -65,15 +65,21 @@ bool encode_bf16(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// k blocks (64 wide) per phase-1 unit: 32 -> 512 KB of W2 per unit.
-int kb2_per_unit() {
-  static int v = 0;
-  if (!v) {
+// k blocks (64 wide) per phase-1 unit.  Default: the down projection split
+// in two halves (at least 32 blocks), so the expert stream ends in
+// 2*tiles2 units per segment and K4 sums two partial slots.  Measured on
+// B200 at Mixtral shape (kb2_total = 224): split 2 beat 3, 4, 7, 14 and 1 by
+// 1.5-5% at T = 32 and 64 (fewer unit transitions and partial writes while
+// the queue still balances); LYNX_KB2_PER overrides it for experiments.
+int kb2_per_unit(int kb2_total) {
+  static int env = -1;
+  if (env < 0) {
     const char* s = getenv("LYNX_KB2_PER");
-    v = s ? atoi(s) : 32;
-    if (v < 1) v = 32;
+    env = s ? atoi(s) : 0;
+    if (env < 0) env = 0;
   }
-  return v;
+  if (env) return env;
+  return std::max(32, (kb2_total + 1) / 2);
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -105,7 +111,7 @@ Geometry geometry(const lynx_layer_t* L, int T) {
   g.kb1 = (L->d_model + 63) / 64;
   g.tiles2 = (L->d_model + 127) / 128;
   g.kb2_total = (L->d_ff + 63) / 64;
-  g.kb2_per = std::min(g.kb2_total, kb2_per_unit());
+  g.kb2_per = std::min(g.kb2_total, kb2_per_unit(g.kb2_total));
   g.split2 = (g.kb2_total + g.kb2_per - 1) / g.kb2_per;
   const int rows = std::min(T, LYNX_SEG_ROWS);
   g.bn = rows <= 32 ? 32 : rows <= 64 ? 64 : rows <= 128 ? 128 : 256;
