@@ -226,6 +226,20 @@ __device__ __noinline__ void remap_token(const int32_t* ids, const double* p, in
 // of one CTA; `asg`/`w` may live in shared or global memory.
 __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N, int k,
                                            const PlanOut& o, uint32_t* s_bits, int* s_prefix) {
+  // The plan's pointers in registers: through the `o` reference every global
+  // store below would force a reload of the fields (possible aliasing).
+  int32_t* __restrict__ const o_n_seg = o.n_seg;
+  int32_t* __restrict__ const o_n_used = o.n_used;
+  int32_t* __restrict__ const o_n_rows = o.n_rows;
+  int32_t* __restrict__ const o_seg_expert = o.seg_expert;
+  int32_t* __restrict__ const o_seg_row = o.seg_row;
+  int32_t* __restrict__ const o_seg_count = o.seg_count;
+  int32_t* __restrict__ const o_seg_order = o.seg_order;
+  int32_t* __restrict__ const o_perm_token = o.perm_token;
+  float* __restrict__ const o_perm_weight = o.perm_weight;
+  int32_t* __restrict__ const o_tok_rows = o.tok_rows;
+  float* __restrict__ const o_tok_weight = o.tok_weight;
+  int* __restrict__ const o_counters = o.counters;
   __shared__ int s_cnt[LYNX_MAX_EXPERTS];
   __shared__ int s_base[LYNX_MAX_EXPERTS];
   __shared__ int s_shared_base;
@@ -257,7 +271,7 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     s_cnt[e] = run;
   }
   #pragma unroll 1
-  for (int i = tid; i < o.n_counters; i += nthr) o.counters[i] = 0;
+  for (int i = tid; i < o.n_counters; i += nthr) o_counters[i] = 0;
   __syncthreads();
   if (tid < 32) {
     // Expert bases and segment slots: one warp scans the 16-padded row counts
@@ -295,9 +309,9 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
       #pragma unroll 1
       for (int c = 0; c < nsg[h]; ++c) {
         const int rows = min(LYNX_SEG_ROWS, cnt[h] - c * LYNX_SEG_ROWS);
-        o.seg_expert[seg[h] + c] = e;
-        o.seg_row[seg[h] + c] = base[h] + c * LYNX_SEG_ROWS;
-        o.seg_count[seg[h] + c] = rows;
+        o_seg_expert[seg[h] + c] = e;
+        o_seg_row[seg[h] + c] = base[h] + c * LYNX_SEG_ROWS;
+        o_seg_count[seg[h] + c] = rows;
         if (seg[h] + c < kOrderMax) s_segcnt[seg[h] + c] = rows;
       }
     }
@@ -308,25 +322,25 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     for (int i = lane; i < S * seg_per_shared; i += 32) {
       const int sx = i / seg_per_shared, c = i - sx * seg_per_shared;
       const int rows = min(LYNX_SEG_ROWS, T - c * LYNX_SEG_ROWS);
-      o.seg_expert[seg_off + i] = N + sx;
-      o.seg_row[seg_off + i] = row_off + sx * T16 + c * LYNX_SEG_ROWS;
-      o.seg_count[seg_off + i] = rows;
+      o_seg_expert[seg_off + i] = N + sx;
+      o_seg_row[seg_off + i] = row_off + sx * T16 + c * LYNX_SEG_ROWS;
+      o_seg_count[seg_off + i] = rows;
       if (seg_off + i < kOrderMax) s_segcnt[seg_off + i] = rows;
     }
     if (lane == 0) {
       s_shared_base = row_off;
-      *o.n_seg = seg_off + S * seg_per_shared;
-      *o.n_used = nused + S;
-      *o.n_rows = row_off + S * T16;
+      *o_n_seg = seg_off + S * seg_per_shared;
+      *o_n_used = nused + S;
+      *o_n_rows = row_off + S * T16;
     }
   }
   __syncthreads();
-  if (o.seg_order) {  // K3 queue order: rows desc, segment index asc (largest first)
-    const int nseg = *o.n_seg;  // written by lane 0 above; visible after the barrier
+  if (o_seg_order) {  // K3 queue order: rows desc, segment index asc (largest first)
+    const int nseg = *o_n_seg;  // written by lane 0 above; visible after the barrier
     #pragma unroll 1
     for (int i = tid; i < nseg; i += nthr) {
       if (nseg > kOrderMax) {
-        o.seg_order[i] = i;
+        o_seg_order[i] = i;
         continue;
       }
       const int ci = s_segcnt[i];
@@ -336,7 +350,7 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
         const int cj = s_segcnt[j];
         rank += (cj > ci || (cj == ci && j < i)) ? 1 : 0;
       }
-      o.seg_order[rank] = i;
+      o_seg_order[rank] = i;
     }
   }
   // Per token: its distinct experts ascending (bit scan of a 64-bit set), the
@@ -362,24 +376,24 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
       for (int c = 0; c < LYNX_MAX_TOPK; ++c)
         if (a_r[c] == e) acc += w[t * k + c];
       const float wf = static_cast<float>(acc);
-      o.tok_rows[t * kk + j] = row;
-      o.tok_weight[t * kk + j] = wf;
-      o.perm_token[row] = t;
-      o.perm_weight[row] = wf;
+      o_tok_rows[t * kk + j] = row;
+      o_tok_weight[t * kk + j] = wf;
+      o_perm_token[row] = t;
+      o_perm_weight[row] = wf;
       ++j;
     }
     #pragma unroll 1
     for (; j < k; ++j) {
-      o.tok_rows[t * kk + j] = -1;
-      o.tok_weight[t * kk + j] = 0.f;
+      o_tok_rows[t * kk + j] = -1;
+      o_tok_weight[t * kk + j] = 0.f;
     }
     #pragma unroll 1
     for (int sx = 0; sx < S; ++sx) {
       const int row = s_shared_base + sx * T16 + t;
-      o.tok_rows[t * kk + k + sx] = row;
-      o.tok_weight[t * kk + k + sx] = 1.f;
-      o.perm_token[row] = t;
-      o.perm_weight[row] = 1.f;
+      o_tok_rows[t * kk + k + sx] = row;
+      o_tok_weight[t * kk + k + sx] = 1.f;
+      o_perm_token[row] = t;
+      o_perm_weight[row] = 1.f;
     }
   }
   // zero the 16-row padding of every segment run
@@ -388,15 +402,15 @@ __device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, 
     const int cnt = s_cnt[e];
     #pragma unroll 1
     for (int r = s_base[e] + cnt; r < s_base[e] + ((cnt + 15) & ~15); ++r) {
-      o.perm_token[r] = -1;
-      o.perm_weight[r] = 0.f;
+      o_perm_token[r] = -1;
+      o_perm_weight[r] = 0.f;
     }
   }
   #pragma unroll 1
   for (int i = tid; i < S * (T16 - T); i += nthr) {
     const int row = s_shared_base + (i / (T16 - T)) * T16 + T + i % (T16 - T);
-    o.perm_token[row] = -1;
-    o.perm_weight[row] = 0.f;
+    o_perm_token[row] = -1;
+    o_perm_weight[row] = 0.f;
   }
 }
 
@@ -439,6 +453,8 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   const int T = a.T, N = a.N, k = a.k, tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
   const bool accuracy = a.pol.mode == LYNX_POLICY_ACCURACY;
+  const int floor_keep = a.floor_keep, drop = a.pol.drop_count, budget_cfg = a.pol.freq_keep_budget;
+  const int n_rank_weights = a.pol.n_rank_weights;
   if (accuracy) {  // select_important_tokens
     const double tau = a.pol.confidence_threshold;
     int local = 0;
@@ -500,7 +516,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   SEL_TS_LOCAL(17);
   // Unit votes are integers: order-free atomics are exact.  Rank-weighted
   // votes are float sums and keep numpy's slot order (thread per expert).
-  if (!a.pol.n_rank_weights) {
+  if (!n_rank_weights) {
     #pragma unroll 1
     for (int i = tid; i < T * k; i += nthr)
       if (!accuracy || IMP[i / k]) atomicAdd(&s_icount[IDS[i]], 1);
@@ -558,13 +574,13 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
   __syncthreads();
   SEL_TS_LOCAL(19);
   if (!accuracy) {  // latency_policy
-    const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
-    const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
+    const int room = N - floor_keep > 0 ? N - floor_keep : 0;
+    const int eff = drop < room ? drop : room;
     #pragma unroll 1
     for (int e = tid; e < N; e += nthr) s_keep[e] = s_rank[e] < N - eff;
-    if (tid == 0) *s_clipped = eff != a.pol.drop_count;
+    if (tid == 0) *s_clipped = eff != drop;
   } else {  // accuracy_policy
-    const int budget = a.pol.freq_keep_budget < N ? a.pol.freq_keep_budget : N;
+    const int budget = budget_cfg < N ? budget_cfg : N;
     #pragma unroll 1
     for (int e = tid; e < N; e += nthr) s_keep[e] = (s_counts[e] > 0.0 && s_rank[e] < budget) ? 1 : 0;
     __syncthreads();
@@ -577,7 +593,7 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
       // unkept experts by rank, found with two ballots (N <= 64)
       const bool k0 = lane < N && s_keep[lane], k1 = lane + 32 < N && s_keep[lane + 32];
       const int kept = __popc(__ballot_sync(kFull, k0)) + __popc(__ballot_sync(kFull, k1));
-      const int need = a.floor_keep - kept;
+      const int need = floor_keep - kept;
       if (need > 0) {
         const int e0 = lane < N ? s_order[lane] : -1, e1 = lane + 32 < N ? s_order[lane + 32] : -1;
         const bool u0 = e0 >= 0 && !s_keep[e0], u1 = e1 >= 0 && !s_keep[e1];
