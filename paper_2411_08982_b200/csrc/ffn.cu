@@ -130,6 +130,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Let K4 (combine) launch now: its CTAs are small enough to sit beside this
+  // one and wait in griddepcontrol.wait, so its launch latency leaves the
+  // critical path (K4 still reads nothing before this grid completes).
+  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -341,7 +345,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 #ifdef LYNX_TRACE
   if (threadIdx.x == 0) trace(5, nseg, cta_t0, globaltimer());
 #endif
-  griddep_launch_dependents();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
