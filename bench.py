@@ -449,6 +449,109 @@ def run_stack(args, c):
     }
 
 
+def run_ep_p2p(args, c, rank, world, local_rank):
+    """Expert parallel over NVLink peer memory (ep_p2p.P2PEPLayer): the logits
+    all-gather, dispatch and return are stores issued by the producing
+    kernels into torch symmetric-memory buffers; one CUDA graph per step."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_08982_b200 as L
+    from paper_2411_08982_b200 import ep as EP
+    from paper_2411_08982_b200 import ep_p2p as P2P
+    T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
+    if N % world:
+        raise SystemExit(f"{N} experts do not shard over {world} GPUs")
+    peers = P2P.symmetric_peers(dist.group.WORLD, T, N, d)
+    spec = L.MoEModelSpec(num_layers=1, num_experts=N, top_k=k, d_model=d, d_ff=ff)
+    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
+    layers = []
+    for l in range(n):
+        full = L.build_swiglu_model(spec, seed=100 + l)  # same seed on every rank -> identical model
+        layers.append(P2P.P2PEPLayer(peers, full.router_wt[0].contiguous(), EP.shard_experts(full.w13[0], rank, world),
+                                     EP.shard_experts(full.w2[0], rank, world), N, k, ff, pol))
+        del full
+        torch.cuda.empty_cache()
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    hid = [torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
+    outs = [torch.empty_like(h) for h in hid]
+    for i in range(max(args.warmup, n)):
+        layers[i % n](hid[i % n], outs[i % n])
+    torch.cuda.synchronize()
+    dist.barrier()
+    used_local = []
+    for l in range(n):
+        a = layers[l].assigned_local
+        used_local.append(int((torch.bincount(a[a >= 0].long(), minlength=N // world) > 0).sum()))
+    g_all = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_all):
+        for l in range(n):
+            layers[l](hid[l], outs[l])
+    dist.barrier()
+    g_all.replay()
+    torch.cuda.synchronize()
+    dist.barrier()
+    reps = max(1, args.steps // n)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            g_all.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    steps = reps * n
+    ms = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    crit = torch.tensor([statistics.mean(used_local)], device="cuda")
+    tot = crit.clone()
+    dist.all_reduce(crit, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    # e2e: pinned host input/output per step around the same graphed layers
+    h_host = [h.cpu().pin_memory() for h in hid]
+    o_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for i in range(steps):
+        l = i % n
+        hid[l].copy_(h_host[l], non_blocking=True)
+        layers[l](hid[l], outs[l])
+        o_host.copy_(outs[l], non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    me = torch.tensor([c0.elapsed_time(c1) / steps], device="cuda")
+    dist.all_reduce(me, op=dist.ReduceOp.MAX)
+    ms_e2e = float(me.item())
+    Tg = T * world
+    peak, peak_src = measured_peaks()
+    crit_bytes = float(crit.item()) * SWIGLU_BYTES(c)
+    return {
+        "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
+        "config": {"workload": c["workload"] + f"-ep{world}", "d_model": d, "d_ff": ff, "experts": N,
+                   "top_k": k, "global_batch": Tg, "tokens_per_gpu": T, "policy": policy_name(c),
+                   "parallelism": f"ep{world}", "transport": "nvlink peer memory (lynx_ep_p2p_*, symmetric buffers)",
+                   "weight_copies": n, "mean_used_experts_total": float(tot.item()),
+                   "critical_path_used_experts": float(crit.item())},
+        "roofline": {"bound": "hbm", "kernel": "ffn_kernel per rank (critical path)",
+                     "achieved": crit_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": crit_bytes / (ms * 1e-3) / 1e9 / peak, "peak_source": peak_src,
+                     "note": "critical-path bytes / whole step time (includes the peer-memory exchanges)",
+                     "traffic": None},
+        "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
+        "gpu_launches": 11 * steps,
+        "clocks": clocks.summary(),
+    }
+
+
 def run_ep(args, c, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -547,6 +650,8 @@ def main():
     ap.add_argument("--impl", choices=["lynx", "reference"], default="lynx")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep-transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1: expert-parallel exchange over NVLink peer memory or NCCL collectives")
     ap.add_argument("--tokens", type=int, default=None, help="override the config's batch (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -567,7 +672,16 @@ def main():
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        result = run_ep(args, c, rank, world, local_rank)
+        result = None
+        if args.ep_transport == "p2p":
+            try:
+                result = run_ep_p2p(args, c, rank, world, local_rank)
+            except Exception as e:  # symmetric memory unavailable -> NCCL collectives
+                log(f"peer-memory EP unavailable ({type(e).__name__}: {e}); using NCCL collectives")
+                torch.cuda.synchronize()
+                dist.barrier()
+        if result is None:
+            result = run_ep(args, c, rank, world, local_rank)
     elif "layers" in c:
         result = run_stack(args, c)
     else:

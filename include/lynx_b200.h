@@ -281,6 +281,59 @@ int lynx_ep_local_mask(const int32_t *assigned, const double *weights, int T, in
 int lynx_ep_combine(const uint16_t *hidden_local, const float *recv_partial, int T_local, int G,
                     int d, uint16_t *out, lynx_stream_t stream);
 
+/* ---- expert parallel over NVLink peer memory -----------
+ * The fused alternative to the NCCL path above: the logits all-gather, the
+ * token dispatch and the partial-sum return are stores into the peers'
+ * buffers issued by the kernels that produce the data (router, dispatch,
+ * K4), each followed by a release signal per peer; consumers acquire-wait.
+ * Buffers are symmetric (same layout on every rank, e.g. from
+ * torch.distributed._symmetric_memory); the pointer arrays below are DEVICE
+ * arrays of G pointers, the *_local fields this rank's own buffers.
+ *   logits [G*Tl, N] f64    recv [G*Tl, d] bf16    back [G*Tl, d] f32
+ *   flags  [3*G] int32 (zero-initialised)
+ * counters (4 int32) and epoch (1 int32) are this rank's, zero-initialised.
+ * A layer is the four calls in order (route -> dispatch -> expert ->
+ * combine); each call only waits at its start for the previous call's data
+ * of every peer, so ranks may also be driven phase by phase (tests run G
+ * ranks on one GPU that way). */
+typedef struct lynx_ep_peers {
+  int32_t world_size;       /* G */
+  int32_t rank;
+  int32_t tokens_per_rank;  /* Tl */
+  int32_t reserved;
+  double *const *logits;
+  uint16_t *const *recv;
+  float *const *back;
+  int32_t *const *flags;
+  double *logits_local;
+  uint16_t *recv_local;
+  float *back_local;
+  int32_t *flags_local;
+  int32_t *counters;
+  int32_t *epoch;
+} lynx_ep_peers_t;
+
+/* K0 on the local rows into logits_local rows rank*Tl.., then to every peer. */
+int lynx_ep_p2p_route(const uint16_t *router_wt, const uint16_t *hidden_local, int d, int N,
+                      const lynx_ep_peers_t *peers, lynx_stream_t stream);
+/* Wait for every peer's logits; K1 (route + Lynx policy) on the global batch
+ * into `sel` (identical on every rank); dispatch this rank's needed rows into
+ * the owners' recv buffers. */
+int lynx_ep_p2p_dispatch(const uint16_t *hidden_local, int N, int k, int d, int decode,
+                         const lynx_policy_t *policy, const lynx_selection_t *sel,
+                         const lynx_ep_peers_t *peers, lynx_stream_t stream);
+/* Wait for every peer's rows; this rank's experts (local_layer: its N/G
+ * experts, router_wt unused) over recv with the global mask renumbered into
+ * assigned_local/weights_local [G*Tl, k] (caller buffers); K4 stores each
+ * token's partial sum into its owner's back buffer. */
+int lynx_ep_p2p_expert(const lynx_layer_t *local_layer, int N, const int32_t *assigned, const double *weights,
+                       int32_t *assigned_local, double *weights_local, const lynx_ep_peers_t *peers,
+                       void *workspace, size_t workspace_bytes, lynx_stream_t stream);
+/* Wait for every peer's partial sums; out = hidden + sum over ranks (rank
+ * order = experts ascending); advances the epoch. */
+int lynx_ep_p2p_combine(const uint16_t *hidden_local, int d, uint16_t *out, const lynx_ep_peers_t *peers,
+                        lynx_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

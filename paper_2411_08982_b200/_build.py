@@ -21,8 +21,8 @@ BUILD = os.path.join(ROOT, "build")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "liblynx_b200.so")
 
-SOURCES = ["select.cu", "dispatch.cu", "ffn.cu", "attention.cu", "capi.cu"]
-HEADERS = ["ptx.cuh", "lynx_internal.cuh"]
+SOURCES = ["select.cu", "dispatch.cu", "ffn.cu", "attention.cu", "ep_p2p.cu", "capi.cu"]
+HEADERS = ["ptx.cuh", "lynx_internal.cuh", "p2p.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-diag-suppress", "550"]

@@ -68,6 +68,13 @@ class LynxTraceRing(ctypes.Structure):
                                 "flags")]
 
 
+class LynxEPPeers(ctypes.Structure):
+    _fields_ = [("world_size", ctypes.c_int32), ("rank", ctypes.c_int32), ("tokens_per_rank", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)] + [
+        (name, _p) for name in ("logits", "recv", "back", "flags", "logits_local", "recv_local", "back_local",
+                                "flags_local", "counters", "epoch")]
+
+
 class LynxDispatch(ctypes.Structure):
     _fields_ = [(name, _p) for name in (
         "n_seg", "n_used", "n_rows", "seg_expert", "seg_row", "seg_count", "perm_token", "perm_weight",
@@ -95,6 +102,10 @@ _SIGS = {
     "lynx_attention": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_advance_position": (_i, [_p, _i, _p]),
     "lynx_trace_append": (_i, [_p, _p, _i, _p, _p]),
+    "lynx_ep_p2p_route": (_i, [_p, _p, _i, _i, _p, _p]),
+    "lynx_ep_p2p_dispatch": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "lynx_ep_p2p_expert": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "lynx_ep_p2p_combine": (_i, [_p, _i, _p, _p, _p]),
     "lynx_ep_pack": (_i, [_p, _p, _i, _i, _i, _i, _i, _i, _p, _p]),
     "lynx_ep_local_mask": (_i, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p]),
     "lynx_ep_combine": (_i, [_p, _p, _i, _i, _i, _p, _p]),

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "lynx_internal.cuh"
+#include "p2p.cuh"
 
 using namespace lynx;
 
@@ -244,7 +245,8 @@ inline void record(cudaEvent_t const* ev, int i, cudaStream_t s) {
 // K2 gather -> K3 expert GEMM + combine, on a plan already in the workspace.
 // ev (optional): [0] before K2 (gather), [1] before K3 (FFN), [2] before K4 (combine).
 int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_t* out_bf16, float* out_f32,
-                   void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev) {
+                   void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev,
+                   const lynx_ep_peers_t* peers = nullptr) {
   const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff, S = L->num_shared;
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
@@ -298,8 +300,12 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   st = cuda_status(launch_ffn(fp, g.bn, sms, s));
   if (st) return st;
 
-  CombineArgs ca;
-  ca.hidden = out_f32 ? nullptr : hidden;
+  CombineArgs ca{};
+  ca.hidden = (out_f32 || peers) ? nullptr : hidden;
+  if (peers) {
+    ca.peer_mode = 1;
+    ca.peers = *peers;
+  }
   ca.partial = fp.partial;
   ca.slot_stride = static_cast<size_t>(c.rows_cap) * d;
   ca.split2 = g.split2;
@@ -339,17 +345,27 @@ SelectArgs select_args(const double* logits, int T, int N, int k, int decode, co
 
 int moe_forward_common(const lynx_layer_t* layer, const uint16_t* hidden, int T, const int32_t* assigned,
                        const double* weights, uint16_t* out_bf16, float* out_f32, void* workspace,
-                       size_t workspace_bytes, cudaStream_t stream) {
-  int st = check_layer(layer, T, out_f32 != nullptr);
+                       size_t workspace_bytes, cudaStream_t stream, const lynx_ep_peers_t* peers = nullptr) {
+  const bool partial = out_f32 != nullptr || peers != nullptr;
+  int st = check_layer(layer, T, partial);
   if (st) return st;
-  if (out_f32 && layer->num_shared) return LYNX_ERR_UNSUPPORTED;
+  if (partial && layer->num_shared) return LYNX_ERR_UNSUPPORTED;
   const Plan P = plan_for(layer, T, false);
   if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
   void* ws = aligned_ws(workspace);
   st = cuda_status(launch_plan(assigned, weights, T, layer->num_experts, layer->top_k,
                                plan_out(ws, P, layer->num_shared), stream));
   if (st) return st;
-  return gather_and_ffn(layer, hidden, T, out_bf16, out_f32, ws, P, stream, nullptr);
+  return gather_and_ffn(layer, hidden, T, out_bf16, out_f32, ws, P, stream, nullptr, peers);
+}
+
+int check_peers(const lynx_ep_peers_t* P) {
+  if (!P || P->world_size < 1 || P->rank < 0 || P->rank >= P->world_size || P->tokens_per_rank < 1)
+    return LYNX_ERR_SHAPE;
+  if (!P->logits || !P->recv || !P->back || !P->flags || !P->logits_local || !P->recv_local || !P->back_local ||
+      !P->flags_local || !P->counters || !P->epoch)
+    return LYNX_ERR_SHAPE;
+  return LYNX_OK;
 }
 
 int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
@@ -658,6 +674,70 @@ int lynx_ep_combine(const uint16_t* hidden_local, const float* recv_partial, int
                     uint16_t* out, lynx_stream_t stream) {
   if (T_local < 1 || G < 1 || d % 2) return LYNX_ERR_SHAPE;
   return cuda_status(launch_ep_combine(hidden_local, recv_partial, T_local, G, d, out, stream));
+}
+
+int lynx_ep_p2p_route(const uint16_t* router_wt, const uint16_t* hidden_local, int d, int N,
+                      const lynx_ep_peers_t* peers, lynx_stream_t stream) {
+  int st = check_peers(peers);
+  if (st) return st;
+  if (!router_wt || !hidden_local || d < 8 || N < 1 || N % peers->world_size) return LYNX_ERR_SHAPE;
+  if (d % 8 || N > LYNX_MAX_EXPERTS || peers->world_size * peers->tokens_per_rank > LYNX_MAX_TOKENS)
+    return LYNX_ERR_UNSUPPORTED;
+  const int Tl = peers->tokens_per_rank;
+  st = cuda_status(launch_router_logits(hidden_local, router_wt, Tl, d, N,
+                                        peers->logits_local + static_cast<size_t>(peers->rank) * Tl * N, stream));
+  if (st) return st;
+  return cuda_status(launch_ep_put_logits(*peers, N, stream));
+}
+
+int lynx_ep_p2p_dispatch(const uint16_t* hidden_local, int N, int k, int d, int decode, const lynx_policy_t* policy,
+                         const lynx_selection_t* sel, const lynx_ep_peers_t* peers, lynx_stream_t stream) {
+  int st = check_peers(peers);
+  if (st) return st;
+  const int T = peers->world_size * peers->tokens_per_rank;
+  if (!hidden_local || N < 1 || d < 8 || N % peers->world_size) return LYNX_ERR_SHAPE;
+  if (k < 1 || k > N) return LYNX_ERR_TOPK;
+  if (N > LYNX_MAX_EXPERTS || k > LYNX_MAX_TOPK || T > LYNX_MAX_TOKENS || d % 8) return LYNX_ERR_UNSUPPORTED;
+  if (!sel || !sel->expert_ids || !sel->probs || !sel->full_probs || !sel->conf || !sel->assigned ||
+      !sel->weights || !sel->flags)
+    return LYNX_ERR_SHAPE;
+  int floor_keep = k;
+  st = check_policy(policy, k, decode, &floor_keep);
+  if (st) return st;
+  st = cuda_status(launch_ep_wait(*peers, kSigLogits, stream));
+  if (st) return st;
+  SelectArgs a = select_args(peers->logits_local, T, N, k, decode, policy, floor_keep);
+  a.ids = sel->expert_ids;
+  a.probs = sel->probs;
+  a.full = sel->full_probs;
+  st = route_select_common(a, sel, stream);
+  if (st) return st;
+  return cuda_status(launch_ep_dispatch(*peers, hidden_local, sel->assigned, k, N, d, stream));
+}
+
+int lynx_ep_p2p_expert(const lynx_layer_t* local_layer, int N, const int32_t* assigned, const double* weights,
+                       int32_t* assigned_local, double* weights_local, const lynx_ep_peers_t* peers, void* workspace,
+                       size_t workspace_bytes, lynx_stream_t stream) {
+  int st = check_peers(peers);
+  if (st) return st;
+  if (!local_layer || !assigned || !weights || !assigned_local || !weights_local) return LYNX_ERR_SHAPE;
+  const int G = peers->world_size, T = G * peers->tokens_per_rank;
+  if (N % G || local_layer->num_experts * G != N) return LYNX_ERR_SHAPE;
+  st = cuda_status(launch_ep_wait(*peers, kSigDispatch, stream));
+  if (st) return st;
+  st = cuda_status(launch_ep_local_mask(assigned, weights, T, local_layer->top_k, N, G, peers->rank, assigned_local,
+                                        weights_local, stream));
+  if (st) return st;
+  return moe_forward_common(local_layer, peers->recv_local, T, assigned_local, weights_local, nullptr, nullptr,
+                            workspace, workspace_bytes, stream, peers);
+}
+
+int lynx_ep_p2p_combine(const uint16_t* hidden_local, int d, uint16_t* out, const lynx_ep_peers_t* peers,
+                        lynx_stream_t stream) {
+  const int st = check_peers(peers);
+  if (st) return st;
+  if (!hidden_local || !out || d < 2 || d % 2) return LYNX_ERR_SHAPE;
+  return cuda_status(launch_ep_p2p_combine(*peers, hidden_local, d, out, stream));
 }
 
 }  // extern "C"

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "lynx_internal.cuh"
+#include "p2p.cuh"
 
 namespace lynx {
 
@@ -45,7 +46,7 @@ cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
 // accumulation order (simulator.py:101-112) with a fixed split-K order, so
 // the layer output is bit-reproducible.  One CTA per (token, 512 columns);
 // the token's rows are staged once, then all k*S float4 loads issue together.
-__global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
+__global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ CombineArgs a) {
   __shared__ int s_rows[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
   __shared__ float s_w[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
   griddep_launch_dependents();
@@ -56,8 +57,9 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
     s_w[threadIdx.x] = a.tok_weight[t * a.k + threadIdx.x];
   }
   __syncthreads();
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (c >= a.d) return;
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const bool live = c0 < a.d;
+  const int c = live ? c0 : 0;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (a.hidden) {
     const __nv_bfloat162* h =
@@ -99,7 +101,17 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
     }
   }
   const size_t o = static_cast<size_t>(t) * a.d + c;
-  if (a.out_f32) {
+  if (a.peer_mode) {
+    // the token's owner gathers every rank's partial in slot [rank]
+    const int Tl = a.peers.tokens_per_rank;
+    float* dst = a.peers.back[t / Tl] + (static_cast<size_t>(a.peers.rank) * Tl + t % Tl) * a.d + c;
+    if (live) *reinterpret_cast<float4*>(dst) = acc;
+    if (last_cta(a.peers.counters + 1)) {
+      if (threadIdx.x == 0) signal_peers(a.peers, kSigBack, *a.peers.epoch + 1);
+    }
+  } else if (!live) {
+    return;
+  } else if (a.out_f32) {
     *reinterpret_cast<float4*>(a.out_f32 + o) = acc;
   } else {
     __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(a.out_bf16 + o);

@@ -105,6 +105,8 @@ struct FfnParams {
 // K4: split-K sum + weighted combine (+ residual).
 struct CombineArgs {
   const uint16_t* hidden;  // residual; null -> no residual (EP partial)
+  int peer_mode;           // 1: row t goes to peers.back[t / Tl] rows rank*Tl + t % Tl, then signal
+  lynx_ep_peers_t peers;
   const float* partial;    // [split2][rows_cap][d]
   size_t slot_stride;      // rows_cap * d
   int split2, T, k, d;  // k = entries per token in tok_rows (top_k + shared)
@@ -140,6 +142,13 @@ cudaError_t launch_advance_position(int32_t* pos, int by, cudaStream_t s);
 
 cudaError_t launch_trace_append(const lynx_trace_ring_t& r, const int32_t* pos, int layer,
                                 const lynx_selection_t& sel, cudaStream_t s);
+
+cudaError_t launch_ep_put_logits(const lynx_ep_peers_t& P, int N, cudaStream_t s);
+cudaError_t launch_ep_wait(const lynx_ep_peers_t& P, int kind, cudaStream_t s);
+cudaError_t launch_ep_dispatch(const lynx_ep_peers_t& P, const uint16_t* hidden_local, const int32_t* assigned, int k,
+                               int N, int d, cudaStream_t s);
+cudaError_t launch_ep_p2p_combine(const lynx_ep_peers_t& P, const uint16_t* hidden_local, int d, uint16_t* out,
+                                  cudaStream_t s);
 
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s);

@@ -170,3 +170,40 @@ def test_forward_partial_empty_shard_is_zero():
     weights = torch.zeros((T, 2), dtype=torch.float64, device="cuda")
     out = L.forward_partial(hidden, model, 0, assigned, weights)
     assert torch.count_nonzero(out).item() == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,N,policy", [(2, 8, ("latency", 4)), (4, 8, ("accuracy", 3)), (8, 8, ("latency", 4)),
+                                        (4, 16, ("latency", 6))])
+def test_p2p_ep_simulated_ranks_match_single_device(G, N, policy):
+    """Peer-memory EP (lynx_ep_p2p_*) with G ranks simulated on one GPU:
+    every rank's selection is bit-identical to the single-device layer on the
+    global batch, and its output rows match that layer's rows (bf16 tol; the
+    cross-rank sum reorders the fp32 additions)."""
+    import torch
+
+    import paper_2411_08982_b200 as L
+    from paper_2411_08982_b200 import ep as EP
+    from paper_2411_08982_b200 import ep_p2p as P2P
+    Tl, k, d, ff = 16, 2, 256, 512
+    spec = L.MoEModelSpec(1, N, k, d, ff)
+    model = L.build_swiglu_model(spec, seed=G + N)
+    mode, x = policy
+    cfg = L.PolicyConfig(mode=mode, drop_count=x if mode == "latency" else 0,
+                         freq_keep_budget=x if mode == "accuracy" else 4)
+    hidden = torch.randn((G * Tl, d), device="cuda").to(torch.bfloat16)
+    ref_layer = L.LynxMoELayer(model, 0, G * Tl, policy=cfg)
+    ref = ref_layer(hidden)
+    peers = P2P.simulated_peers(G, Tl, N, d)
+    layers = [P2P.P2PEPLayer(peers[r], model.router_wt[0], EP.shard_experts(model.w13[0], r, G),
+                             EP.shard_experts(model.w2[0], r, G), N, k, ff, cfg) for r in range(G)]
+    hs = [hidden[r * Tl:(r + 1) * Tl].contiguous() for r in range(G)]
+    for step in range(2):  # second step exercises the epoch advance
+        outs = P2P.run_simulated(layers, hs)
+        torch.cuda.synchronize()
+        for r in range(G):
+            assert torch.equal(layers[r].assigned, ref_layer.assigned), (step, r)
+            assert O.norm_rel_err(outs[r].float().cpu().numpy(), ref[r * Tl:(r + 1) * Tl].float().cpu().numpy()) <= 1e-2
+            delta = (outs[r].float() - hs[r].float()).cpu().numpy()
+            ref_delta = (ref[r * Tl:(r + 1) * Tl].float() - hs[r].float()).cpu().numpy()
+            assert O.norm_rel_err(delta, ref_delta) <= 3e-2, (step, r)
