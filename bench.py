@@ -452,7 +452,7 @@ def run_stack(args, c):
 def run_ep_p2p(args, c, rank, world, local_rank):
     """Expert parallel over NVLink peer memory (ep_p2p.P2PEPLayer): the logits
     all-gather, dispatch and return are stores issued by the producing
-    kernels into torch symmetric-memory buffers; one CUDA graph per step."""
+    kernels into the peers' CUDA-IPC-shared buffers; one CUDA graph per step."""
     import torch
     import torch.distributed as dist
 
@@ -462,7 +462,7 @@ def run_ep_p2p(args, c, rank, world, local_rank):
     T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
     if N % world:
         raise SystemExit(f"{N} experts do not shard over {world} GPUs")
-    peers = P2P.symmetric_peers(dist.group.WORLD, T, N, d)
+    peers = P2P.ipc_peers(dist.group.WORLD, T, N, d)
     spec = L.MoEModelSpec(num_layers=1, num_experts=N, top_k=k, d_model=d, d_ff=ff)
     pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
     layers = []
@@ -537,7 +537,7 @@ def run_ep_p2p(args, c, rank, world, local_rank):
         "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
         "config": {"workload": c["workload"] + f"-ep{world}", "d_model": d, "d_ff": ff, "experts": N,
                    "top_k": k, "global_batch": Tg, "tokens_per_gpu": T, "policy": policy_name(c),
-                   "parallelism": f"ep{world}", "transport": "nvlink peer memory (lynx_ep_p2p_*, symmetric buffers)",
+                   "parallelism": f"ep{world}", "transport": "nvlink peer memory (lynx_ep_p2p_*, CUDA-IPC shared buffers)",
                    "weight_copies": n, "mean_used_experts_total": float(tot.item()),
                    "critical_path_used_experts": float(crit.item())},
         "roofline": {"bound": "hbm", "kernel": "ffn_kernel per rank (critical path)",

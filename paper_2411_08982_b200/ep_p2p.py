@@ -13,10 +13,11 @@ acquire-wait on the flags (include/lynx_b200.h, ``lynx_ep_p2p_*``):
             token's partial sum into its owner's back buffer
   combine   wait partials; residual + sum over ranks (rank order)
 
-Buffers come from ``torch.distributed._symmetric_memory`` across processes
-(``symmetric_peers``), or -- for tests on one GPU -- from ordinary device
-allocations shared by G simulated ranks (``simulated_peers``), which run the
-same kernels on plain device pointers and are driven phase by phase.
+Buffers are shared across processes over CUDA IPC (``ipc_peers``: one GPU
+per rank over NVLink, or several processes on one GPU), or through
+``torch.distributed._symmetric_memory`` (``symmetric_peers``, distinct GPUs
+only).  For single-process tests, G simulated ranks share ordinary device
+allocations (``simulated_peers``) and are driven phase by phase.
 """
 
 from __future__ import annotations
@@ -99,6 +100,37 @@ def symmetric_peers(group, Tl: int, N: int, d: int) -> PeerSet:
     dist.barrier(group)
     zeros = lambda shape, dt: torch.zeros(shape, dtype=dt, device="cuda")  # noqa: E731
     return _make(G, rank, Tl, bufs, arrays, zeros((4,), torch.int32), zeros((1,), torch.int32))
+
+
+def ipc_peers(group, Tl: int, N: int, d: int) -> PeerSet:
+    """This process's rank with buffers shared over CUDA IPC (cudaIpc*MemHandle
+    through torch's storage sharing): works across GPUs of one node (the
+    opened peer allocations are reached over NVLink) and for several
+    processes on one GPU, which is how it is tested here."""
+    torch = _torch()
+    import torch.distributed as dist
+    G, rank = dist.get_world_size(group), dist.get_rank(group)
+    zeros = lambda shape, dt: torch.zeros(shape, dtype=dt, device="cuda")  # noqa: E731
+    bufs = _buffers(zeros, G, Tl, N, d)
+    torch.cuda.synchronize()
+    mine = {n: t.untyped_storage()._share_cuda_() for n, t in bufs.items()}
+    allh = [None] * G
+    dist.all_gather_object(allh, mine, group=group)
+    opened, arrays = [], {}
+    for n, t in bufs.items():
+        ptrs = []
+        for r in range(G):
+            if r == rank:
+                ptrs.append(t.data_ptr())
+                continue
+            st = torch.UntypedStorage._new_shared_cuda(*allh[r][n])
+            opened.append(st)
+            ptrs.append(st.data_ptr())
+        arrays[n] = _ptr_array(ptrs)
+    dist.barrier(group)
+    ps = _make(G, rank, Tl, bufs, arrays, zeros((4,), torch.int32), zeros((1,), torch.int32))
+    ps.keep = ps.keep + (opened,)
+    return ps
 
 
 class P2PEPLayer:
@@ -188,5 +220,5 @@ def run_simulated(layers: list, hiddens: list) -> list:
     return [lay.combine(h) for lay, h in zip(layers, hiddens)]
 
 
-__all__ = ["P2PEPLayer", "PeerSet", "simulated_peers", "symmetric_peers", "run_simulated"]
+__all__ = ["P2PEPLayer", "PeerSet", "simulated_peers", "symmetric_peers", "ipc_peers", "run_simulated"]
 del ctypes

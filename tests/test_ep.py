@@ -207,3 +207,19 @@ def test_p2p_ep_simulated_ranks_match_single_device(G, N, policy):
             delta = (outs[r].float() - hs[r].float()).cpu().numpy()
             ref_delta = (ref[r * Tl:(r + 1) * Tl].float() - hs[r].float()).cpu().numpy()
             assert O.norm_rel_err(delta, ref_delta) <= 3e-2, (step, r)
+
+
+@pytest.mark.gpu
+def test_p2p_ep_two_processes_one_gpu():
+    """The multi-process wiring (CUDA-IPC buffer exchange, cross-process
+    release/acquire flags, epochs): two torchrun ranks on one GPU run three
+    layer steps of the peer-memory EP layer against the single-device layer."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "scripts",
+                                                                                          "p2p_two_proc.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "rank 0: ok" in out.stdout and "rank 1: ok" in out.stdout
