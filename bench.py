@@ -650,6 +650,8 @@ def main():
     ap.add_argument("--impl", choices=["lynx", "reference"], default="lynx")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N>1 on ONE GPU (gloo + CUDA IPC): functional check only, not a measurement")
     ap.add_argument("--ep-transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1: expert-parallel exchange over NVLink peer memory or NCCL collectives")
     ap.add_argument("--tokens", type=int, default=None, help="override the config's batch (diagnostics)")
@@ -667,11 +669,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:  # functional check of the N>1 path with every rank on GPU 0 (timings meaningless)
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         result = None
         if args.ep_transport == "p2p":
             try:
