@@ -68,3 +68,18 @@ def has_gpu() -> bool:
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def load_simulate_golden():
+    """tests/golden/simulate.npz + .json (make_golden_simulate.py): the
+    reference's simulate() on a bf16-rounded model, per case and event."""
+    data = np.load(os.path.join(GOLDEN, "simulate.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "simulate.json")))
+    w = {k[2:]: data[k] for k in data.files if k.startswith("w_")}
+    cases = []
+    for ci, c in enumerate(meta["cases"]):
+        evs = []
+        for ei, em in enumerate(c["events"]):
+            evs.append(dict(em, **{f: data[f"c{ci}_e{ei}_{f}"] for f in ("ids", "assigned", "weights", "retained")}))
+        cases.append(dict(name=c["name"], policy=c["policy"], hidden=data[f"c{ci}_hidden"], events=evs))
+    return meta, w, data["inputs"], cases

@@ -169,3 +169,53 @@ def test_trace_ring_matches_host_records(tmp_path):
     rec.write(path)
     assert L.read_trace_jsonl(path) == got
     assert L.read_masks_jsonl(L.masks_path_for(path)) == rec.mask_records()
+
+
+def test_decode_stack_vs_reference_simulate():
+    """The whole GPU decode stack (attention stand-in + Lynx layer, graphed
+    decode steps, device trace ring) on the reference's own model against
+    the reference's simulate() output (tests/golden/simulate.npz): every
+    routing event's expert ids, assignment and retained set bit-exact, weights
+    to 1e-2 (they come from bf16-state logits), final states within the bf16
+    tolerance of the f64 reference."""
+    from conftest import load_simulate_golden
+    meta, w, x, cases = load_simulate_golden()
+    Ln, N, k, d, ff = meta["L"], meta["N"], meta["k"], meta["d"], meta["ff"]
+
+    class Ref:  # duck-typed moetrim SyntheticMoE
+        pass
+    ref = Ref()
+    ref.spec = L.MoEModelSpec(Ln, N, k, d, ff)
+    ref.router_w, ref.w1, ref.w2 = w["router"], w["1"], w["2"]
+    ref.wq, ref.wk, ref.wv, ref.wo, ref.d_head = w["q"], w["k"], w["v"], w["o"], meta["d_head"]
+    moe = L.from_reference(ref)
+    attn = L.attention_from_reference(ref)
+    for case in cases:
+        p = case["policy"]
+        pol = None if p is None else L.PolicyConfig(**{f: (tuple(v) if isinstance(v, list) else v)
+                                                       for f, v in p.items()})
+        rec = L.TraceRecorder("golden", Ln, meta["B"], N, k, capacity=8)
+        stack = L.DecodeStack(moe, attn, meta["B"], max_len=16, policy=pol, trace=rec)
+        out = stack.simulate(x, meta["steps"]).hidden
+        assert O.norm_rel_err(f64(out), case["hidden"]) <= 2e-2, case["name"]
+        got = {}
+        for r in rec.records():
+            got.setdefault((r.batch_id, r.layer), []).append(r)
+        for ev in case["events"]:
+            recs = sorted(got[(ev["event"], ev["layer"])], key=lambda r: (r.token_id, r.rank))
+            T = len(recs) // k
+            ids = np.array([r.expert_original for r in recs]).reshape(T, k)
+            asg = np.array([r.expert_assigned for r in recs]).reshape(T, k)
+            wts = np.array([r.weight for r in recs]).reshape(T, k)
+            tag = (case["name"], ev["event"], ev["layer"])
+            assert np.array_equal(ids, ev["ids"]), tag
+            assert np.array_equal(asg, ev["assigned"]), tag
+            assert np.allclose(wts, ev["weights"], atol=1e-2), tag
+            ref_t = sorted(ev["trace"], key=lambda r: (r["token_id"], r["rank"]))
+            assert [(r["token_id"], r["rank"], r["expert_original"], r["expert_assigned"]) for r in ref_t] == \
+                [(r.token_id, r.rank, r.expert_original, r.expert_assigned) for r in recs], tag
+        masks = {(m.batch_id, m.layer): m for m in rec.mask_records()}
+        for ev in case["events"]:
+            m, rm = masks[(ev["event"], ev["layer"])], ev["mask"]
+            assert list(m.retained) == list(rm["retained"]) and m.clipped == rm["clipped"], ev
+            assert m.num_tokens == rm["num_tokens"] and m.num_important == rm["num_important"], ev
