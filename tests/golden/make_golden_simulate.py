@@ -25,7 +25,7 @@ import numpy as np
 from moetrim import simulator as sim
 from moetrim.policy import PolicyConfig
 from moetrim.router import MoEModelSpec
-from moetrim.trace import mask_record_from_event, records_from_event
+from moetrim.trace import mask_record_from_event, records_from_event, write_masks_jsonl, write_trace_jsonl
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
@@ -102,6 +102,12 @@ def main():
                             "trace": rec, "mask": mrec})
         meta["cases"].append({"name": name, "policy": None if cfg is None else dataclasses.asdict(cfg),
                               "events": ev_meta})
+    # the reference's own JSONL files for case 0 (byte-level schema check of trace.py)
+    _, events = run(model, x, CASES[0][1])
+    recs = [r for (e, l, ph, sel, m) in events for r in records_from_event("golden", e, l, ph, sel, m)]
+    write_trace_jsonl(os.path.join(HERE, "simulate_trace.jsonl"), recs)
+    write_masks_jsonl(os.path.join(HERE, "simulate_trace.masks.jsonl"),
+                      [mask_record_from_event("golden", e, l, ph, m) for (e, l, ph, sel, m) in events])
     np.savez_compressed(os.path.join(HERE, "simulate.npz"), **flat)
     with open(os.path.join(HERE, "simulate.json"), "w") as f:
         json.dump(meta, f, indent=0)

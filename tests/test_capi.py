@@ -78,3 +78,23 @@ def test_product_path_fails_loudly_without_library(tmp_path):
             _native.load(str(tmp_path / "missing.so"))
     finally:
         _native._lib = saved
+
+
+def test_new_entry_points_validate_without_gpu():
+    """Decode-stack, trace-ring and peer-memory EP entry points reject bad
+    arguments before touching CUDA."""
+    from paper_2411_08982_b200 import _native
+    lib = _native.load()
+    assert lib.lynx_attention(None, None, 1, 1, 0, None, None, None, 0, None) == -1
+    a = _native.LynxAttention(d_model=4096, d_head=128, max_len=8, wqkv=1, wo=1, k_cache=1, v_cache=1)
+    ref = lambda s: ctypes.cast(ctypes.pointer(s), ctypes.c_void_p)  # noqa: E731
+    assert lib.lynx_attention(ref(a), 1, 2, 1, 0, 1, 1, 1, 1 << 20, None) == -7  # d_head > LYNX_MAX_DHEAD
+    a.d_head = 16
+    assert lib.lynx_attention(ref(a), 1, 2, 1, 0, 1, 1, 1, 0, None) == -8        # workspace too small
+    assert lib.lynx_attention_workspace_bytes(64, 16) >= 64 * 16 * 4
+    assert lib.lynx_advance_position(None, 1, None) == -1
+    assert lib.lynx_trace_append(None, None, 0, None, None) == -1
+    assert lib.lynx_ep_p2p_route(None, None, 4096, 8, None, None) == -1
+    p = _native.LynxEPPeers(world_size=2, rank=2, tokens_per_rank=4)
+    assert lib.lynx_ep_p2p_combine(1, 4096, 1, ref(p), None) == -1             # rank out of range
+    assert lib.lynx_ep_p2p_dispatch(1, 8, 2, 4096, 1, None, None, None, None) == -1
