@@ -251,3 +251,72 @@ def test_stream_host_matches_device_calls():
     torch.cuda.synchronize()
     for h, o in zip(hs, outs):
         assert torch.equal(o, layer(h.cuda()).cpu())
+
+
+# ---- the reference's forward_layer known answers (test_simulator.py:71-125),
+# embedded at d = ff = 8 (the kernels need 16-byte rows): the reference's
+# 2x2 blocks sit top-left, the padding is zero, so columns 0-1 carry the
+# reference's numbers and the rest stay equal to the input.
+def _embed_model(w1_blocks, w2_blocks, N, k, d=8):
+    class Ref:  # duck-typed SyntheticMoE
+        pass
+    ref = Ref()
+    ref.spec = L.MoEModelSpec(1, N, k, d, d)
+    ref.w1 = np.zeros((1, N, d, d))
+    ref.w2 = np.zeros((1, N, d, d))
+    ref.w1[0, :, :2, :2] = w1_blocks
+    ref.w2[0, :, :2, :2] = w2_blocks
+    ref.router_w = np.zeros((1, d, N))
+    return L.from_reference(ref)
+
+
+def _mask(assigned, weights, N):
+    a = torch.as_tensor(np.asarray(assigned), dtype=torch.int32).cuda()
+    return L.ExpertMask(layer_index=0, phase=L.Phase.DECODE, retained=torch.arange(N).cuda(), remap_original=a,
+                        remap_assigned=a, remap_weights=torch.as_tensor(np.asarray(weights, dtype=np.float64)).cuda())
+
+
+def _hid(rows, d=8):
+    h = np.zeros((len(rows), d))
+    h[:, :2] = rows
+    return torch.from_numpy(h).float().cuda().to(torch.bfloat16)
+
+
+def test_reference_hand_computed_forward():
+    """test_simulator.py:71-83: token 0 -> expert 0 gives h + 0.5 tanh(h),
+    token 1 -> expert 1 gives h + swap(tanh(2h))."""
+    model = _embed_model(np.stack([np.eye(2), 2 * np.eye(2)]), np.stack([0.5 * np.eye(2), [[0, 1], [1, 0]]]), 2, 1)
+    hidden = _hid([[1.0, 0.0], [0.0, 1.0]])
+    y = _np(L.forward_layer(hidden, model, 0, _mask([[0], [1]], [[1.0], [1.0]], 2)))
+    h = np.array([[1.0, 0.0], [0.0, 1.0]])
+    exp0 = h[0] + 0.5 * np.tanh(h[0])
+    exp1 = h[1] + np.tanh(2.0 * h[1]) @ np.array([[0.0, 1.0], [1.0, 0.0]])
+    assert np.allclose(y[0, :2], exp0, atol=1e-2) and np.allclose(y[1, :2], exp1, atol=1e-2)
+    assert np.all(y[:, 2:] == 0)
+
+
+def test_reference_collapsed_slots_apply_expert_once():
+    """test_simulator.py:94-118: remap onto retained {1} with k=2 collapses
+    both slots onto expert 1; the expert runs once with the merged weight 1."""
+    rng = np.random.default_rng(3)
+    w1 = rng.normal(size=(4, 2, 2))
+    w2 = rng.normal(size=(4, 2, 2))
+    model = _embed_model(w1, w2, 4, 2)
+    logits = rng.normal(size=(3, 4))
+    sel = L.route_batch(L.RoutingLogits(0, L.Phase.DECODE, logits), 2)
+    _, assigned, weights = L.remap_tokens(sel, np.array([1]))
+    assert torch.all(assigned == 1)
+    hx = rng.normal(size=(3, 2))
+    hidden = _hid(hx)
+    y = _np(L.forward_layer(hidden, model, 0, _mask(assigned.cpu().numpy(), weights.cpu().numpy(), 4)))
+    hb = _np(hidden)[:, :2].astype(np.float64)
+    f = lambda a: O.bf16_round(np.asarray(a, dtype=np.float32)).astype(np.float64)  # noqa: E731
+    ref = hb + np.tanh(hb @ f(w1[1])) @ f(w2[1])
+    assert O.norm_rel_err(y[:, :2], ref) <= 1e-2
+
+
+def test_forward_rejects_token_mismatch():
+    """test_simulator.py:120-125: mask rows != hidden rows -> ValidationError."""
+    model = _embed_model(np.stack([np.eye(2), np.eye(2)]), np.stack([np.eye(2), np.eye(2)]), 2, 1)
+    with pytest.raises(L.ValidationError):
+        L.forward_layer(_hid([[1.0, 0.0], [0.0, 1.0]]), model, 0, _mask([[0]], [[1.0]], 2))
