@@ -436,7 +436,7 @@ def run_stack(args, c):
                    f"{N - c['drop']})", "parallelism": "single", "prefill_len": P, "d_head": c["d_head"],
                    "l2": "inputs > L2: each step streams every layer's used experts (>= 45 GB) >> 126 MB L2",
                    "budget_sweep": sweep},
-        "roofline": {"bound": "hbm", "kernel": "whole decode step (32 x [attention, K0..K4])",
+        "roofline": {"bound": "hbm", "kernel": "whole decode step (32 x [attention + fused router, K1..K4])",
                      "achieved": best["achieved_gbs"], "peak": peak, "unit": "GB/s",
                      "frac": best["achieved_gbs"] / peak, "peak_source": peak_src,
                      "frac_of_8TBs": best["achieved_gbs"] / 8000.0, "algorithmic_bytes_per_step": best["step_bytes"],
@@ -444,7 +444,7 @@ def run_stack(args, c):
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": B * d * 2, "d2h_bytes_per_step": B * d * 2,
                 "api": "paper_2411_08982_b200.DecodeStack.step (one CUDA graph per step)"},
-        "gpu_launches": (nl * 7 + 1) * args.steps,
+        "gpu_launches": (nl * (6 if head.fused_router else 7) + 1) * args.steps,
         "clocks": clocks,
     }
 

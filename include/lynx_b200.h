@@ -201,6 +201,12 @@ int lynx_moe_layer(const lynx_layer_t *layer, const uint16_t *hidden, int T, int
                    const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,
                    void *workspace, size_t workspace_bytes, lynx_stream_t stream);
 
+/* lynx_moe_layer with the router logits given (f64 [T, N], e.g. from the
+ * fused router of lynx_attention): K1..K4 only. */
+int lynx_moe_layer_logits(const lynx_layer_t *layer, const uint16_t *hidden, const double *logits, int T,
+                          int decode, const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,
+                          void *workspace, size_t workspace_bytes, lynx_stream_t stream);
+
 /* lynx_moe_layer that also records caller-created CUDA events (cudaEvent_t)
  * on `stream` around each kernel: events[0] before K0 (router), [1] before
  * K1 (select + plan), [2] before K2 (gather), [3] before K3 (expert FFN with
@@ -231,13 +237,22 @@ typedef struct lynx_attention {
   int32_t d_model;          /* d (multiple of 8) */
   int32_t d_head;           /* dh <= LYNX_MAX_DHEAD */
   int32_t max_len;          /* cache capacity in positions */
-  int32_t reserved;
+  int32_t num_experts;      /* N of the fused router (router_wt != NULL), <= LYNX_MAX_FUSED_ROUTER */
   const uint16_t *wqkv;     /* [3*dh, d] bf16: wq^T, wk^T, wv^T (reference [d, dh] each, simulator.py:35-37) */
   const uint16_t *wo;       /* [dh, d] bf16 (reference wo, simulator.py:38) */
   float *k_cache;           /* [B, max_len, dh] f32 */
   float *v_cache;           /* [B, max_len, dh] f32 */
+  /* Optional router fused into the attention output: the
+   * next MoE layer's logits rms_norm(h_out) . router (simulator.py:82-83)
+   * are produced by the same kernel that produces h_out, written to
+   * logits [B*Tn, N] f64; feed them to lynx_moe_layer_logits.  NULL = off. */
+  const uint16_t *router_wt;  /* [N, d] bf16 */
+  double *logits;             /* [B*Tn, N] f64 */
 } lynx_attention_t;
 
+#define LYNX_MAX_FUSED_ROUTER 16
+
+/* q scratch plus, with the fused router, per-chunk partials and row counters. */
 size_t lynx_attention_workspace_bytes(int rows, int d_head);
 int lynx_attention(const lynx_attention_t *attn, const uint16_t *h_in, int B, int Tn, int norm_input,
                    const int32_t *pos, uint16_t *h_out, void *workspace, size_t workspace_bytes,

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get(
 
 # include/lynx_b200.h constants
 LYNX_OK = 0
-ABI_VERSION = 3
+ABI_VERSION = 4
 STATUS = {
     -1: "invalid shape", -2: "k out of range", -3: "min_experts must be >= top_k",
     -4: "retained set empty or out of range", -5: "token count mismatch", -6: "CUDA error",
@@ -27,6 +27,7 @@ STATUS = {
 VALIDATION_CODES = {-1, -2, -3, -4, -5, -7, -9}
 FLAG_CLIPPED, FLAG_NONFINITE, FLAG_ZERO_MASS = 1, 2, 4
 MAX_EXPERTS, MAX_TOPK, MAX_TOKENS, SEG_ROWS, MAX_SHARED, MAX_DHEAD = 64, 8, 4096, 256, 4, 64
+MAX_FUSED_ROUTER = 16
 POLICY_NONE, POLICY_LATENCY, POLICY_ACCURACY = 0, 1, 2
 CONF_TOP1, CONF_MARGIN = 0, 1
 ACT_SWIGLU, ACT_TANH2 = 0, 1
@@ -58,7 +59,8 @@ class LynxLayer(ctypes.Structure):
 
 class LynxAttention(ctypes.Structure):
     _fields_ = [("d_model", ctypes.c_int32), ("d_head", ctypes.c_int32), ("max_len", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("wqkv", _p), ("wo", _p), ("k_cache", _p), ("v_cache", _p)]
+                ("num_experts", ctypes.c_int32), ("wqkv", _p), ("wo", _p), ("k_cache", _p), ("v_cache", _p),
+                ("router_wt", _p), ("logits", _p)]
 
 
 class LynxTraceRing(ctypes.Structure):
@@ -96,6 +98,7 @@ _SIGS = {
     "lynx_moe_forward": (_i, [_p, _p, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_forward_partial": (_i, [_p, _p, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_layer": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "lynx_moe_layer_logits": (_i, [_p, _p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_layer_profiled": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p, _p, _i]),
     "lynx_pack_w13": (_i, [_p, _p, _i, _i, _i, _p, _p]),
     "lynx_attention_workspace_bytes": (ctypes.c_size_t, [_i, _i]),

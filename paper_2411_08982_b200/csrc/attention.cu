@@ -125,6 +125,63 @@ __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_con
   }
 }
 
+// Fused router: rms_norm(h_out) . W_r (simulator.py:26-27,
+// 82-83) for the row this CTA writes part of.  Each CTA reduces its 1024
+// columns' partial dots and sum of squares; the row's last CTA sums the
+// chunks in chunk order (deterministic) and writes the f64 logits the way
+// K0 does: dot * 1 / sqrt(ss / d + 1e-12).
+__device__ __forceinline__ void fused_router(const AttnArgs& a, int row, const float (&x)[4],
+                                             const uint2 (&rw)[LYNX_MAX_FUSED_ROUTER]) {
+  __shared__ float red2[kAttnThreads / 32][LYNX_MAX_FUSED_ROUTER + 1];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int N = a.N, chunks = gridDim.y, chunk = blockIdx.y;
+  const bool live = blockIdx.y * kOutCols + threadIdx.x * 4 < a.d;
+  float v = x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kAll, v, off);
+  if (lane == 0) red2[warp][N] = v;
+#pragma unroll
+  for (int e = 0; e < LYNX_MAX_FUSED_ROUTER; ++e) {
+    if (e >= N) break;
+    float dot = 0.f;
+    if (live) {
+      const float2 w0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rw[e].x));
+      const float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rw[e].y));
+      dot = x[0] * w0.x + x[1] * w0.y + x[2] * w1.x + x[3] * w1.y;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(kAll, dot, off);
+    if (lane == 0) red2[warp][e] = dot;
+  }
+  __syncthreads();
+  float* part = a.rpart + (static_cast<size_t>(row) * chunks + chunk) * (N + 1);
+  if (threadIdx.x <= N) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red2[w][threadIdx.x];
+    part[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int t = atomicAdd(&a.row_arrivals[row], 1);
+    s_last = t == chunks - 1;
+    if (s_last) a.row_arrivals[row] = 0;  // re-armed for the next launch
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < N) {
+    __threadfence();
+    const float* rp = a.rpart + static_cast<size_t>(row) * chunks * (N + 1);
+    float dot = 0.f, ss = 0.f;
+    for (int c = 0; c < chunks; ++c) {
+      dot += __ldcg(rp + c * (N + 1) + threadIdx.x);
+      ss += __ldcg(rp + c * (N + 1) + N);
+    }
+    const double inv = 1.0 / sqrt(static_cast<double>(ss) / a.d + 1e-12);
+    a.logits[static_cast<size_t>(row) * N + threadIdx.x] = static_cast<double>(dot) * inv;
+  }
+}
+
 __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ float sm[];  // K chunk | V chunk | scores chunk | ctx partials
   __shared__ float red[32];
@@ -145,11 +202,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   const uint16_t* hrow = a.h_in + static_cast<size_t>(row) * a.d;
   uint2 hres = make_uint2(0, 0);
   uint2 wo[kWoPrefetch];  // the first kWoPrefetch head rows of Wo (all of them at the reference's dh = 16)
+  uint2 rw[LYNX_MAX_FUSED_ROUTER];  // fused router: this thread's 4 columns of every expert's router row
   if (live) {
     hres = __ldg(reinterpret_cast<const uint2*>(hrow + col));
 #pragma unroll
     for (int c = 0; c < kWoPrefetch; ++c)
       if (c < dh) wo[c] = __ldg(reinterpret_cast<const uint2*>(a.wo + static_cast<size_t>(c) * a.d + col));
+    if (a.router_wt) {
+#pragma unroll
+      for (int e = 0; e < LYNX_MAX_FUSED_ROUTER; ++e)
+        if (e < a.N) rw[e] = __ldg(reinterpret_cast<const uint2*>(a.router_wt + static_cast<size_t>(e) * a.d + col));
+    }
   }
   if (threadIdx.x < dh) qs[threadIdx.x] = a.q[static_cast<size_t>(row) * dh + threadIdx.x];
   const int total = *a.pos + i + 1;  // causal: cache positions 0 .. pos+i
@@ -205,6 +268,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
     ctx[threadIdx.x] = acc / l_run;
   }
   __syncthreads();
+  float rout[4] = {0.f, 0.f, 0.f, 0.f};
   if (live) {
     float o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -233,7 +297,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
     *reinterpret_cast<__nv_bfloat162*>(&out.x) = __floats2bfloat162_rn(h0.x * s1 + o[0], h0.y * s1 + o[1]);
     *reinterpret_cast<__nv_bfloat162*>(&out.y) = __floats2bfloat162_rn(h1.x * s1 + o[2], h1.y * s1 + o[3]);
     *reinterpret_cast<uint2*>(a.h_out + static_cast<size_t>(row) * a.d + col) = out;
+    if (a.router_wt) {
+      // the next layer's router on the values as stored (bf16), like K0
+      const float2 y0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&out.x));
+      const float2 y1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&out.y));
+      rout[0] = y0.x;
+      rout[1] = y0.y;
+      rout[2] = y1.x;
+      rout[3] = y1.y;
+    }
   }
+  if (a.router_wt) fused_router(a, row, rout, rw);
 }
 
 __global__ void advance_position_kernel(int32_t* pos, int by) {

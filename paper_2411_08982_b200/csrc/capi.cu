@@ -21,7 +21,7 @@ using namespace lynx;
 
 namespace {
 
-constexpr int kAbiVersion = 3;
+constexpr int kAbiVersion = 4;
 
 int sm_count_cached() {
   static int cached_dev = -1, cached = 0;
@@ -370,10 +370,10 @@ int check_peers(const lynx_ep_peers_t* P) {
 
 int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
                    uint16_t* out, const lynx_selection_t* sel, void* workspace, size_t workspace_bytes,
-                   cudaStream_t stream, cudaEvent_t const* ev) {
+                   cudaStream_t stream, cudaEvent_t const* ev, const double* given_logits = nullptr) {
   int st = check_layer(layer, T);
   if (st) return st;
-  if (!layer->router_wt) return LYNX_ERR_SHAPE;
+  if (!layer->router_wt && !given_logits) return LYNX_ERR_SHAPE;
   const int N = layer->num_experts, k = layer->top_k;
   int floor_keep = k;
   st = check_policy(policy, k, decode, &floor_keep);
@@ -382,10 +382,14 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   if (!workspace || workspace_bytes < P.total) return LYNX_ERR_WORKSPACE;
   void* ws = aligned_ws(workspace);
 
-  double* logits = at<double>(ws, P.logits);
+  const double* logits = given_logits;
   record(ev, 0, stream);
-  st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, logits, stream));
-  if (st) return st;
+  if (!logits) {
+    double* lg = at<double>(ws, P.logits);
+    st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, lg, stream));
+    if (st) return st;
+    logits = lg;
+  }
 
   SelectArgs a = select_args(logits, T, N, k, decode, policy, floor_keep);
   a.stage = select_can_stage(T, N, k, true) ? 1 : 0;
@@ -594,6 +598,14 @@ int lynx_moe_layer(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   return moe_layer_impl(layer, hidden, T, decode, policy, out, sel, workspace, workspace_bytes, stream, nullptr);
 }
 
+int lynx_moe_layer_logits(const lynx_layer_t* layer, const uint16_t* hidden, const double* logits, int T, int decode,
+                          const lynx_policy_t* policy, uint16_t* out, const lynx_selection_t* sel, void* workspace,
+                          size_t workspace_bytes, lynx_stream_t stream) {
+  if (!logits) return LYNX_ERR_SHAPE;
+  return moe_layer_impl(layer, hidden, T, decode, policy, out, sel, workspace, workspace_bytes, stream, nullptr,
+                        logits);
+}
+
 int lynx_moe_layer_profiled(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode,
                             const lynx_policy_t* policy, uint16_t* out, const lynx_selection_t* sel, void* workspace,
                             size_t workspace_bytes, lynx_stream_t stream, void* const* events, int n_events) {
@@ -608,9 +620,15 @@ int lynx_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, 
   return cuda_status(launch_pack_w13(w1, w3, N, ff, d, w13, stream));
 }
 
+// q scratch | fused-router chunk partials (d <= 8192: <= 8 chunks of N+1 <= 17) | row counters
+constexpr int kRouterChunksMax = 8;
+
 size_t lynx_attention_workspace_bytes(int rows, int d_head) {
   if (rows < 1 || d_head < 1) return 0;
-  return sizeof(float) * static_cast<size_t>(rows) * d_head + 256;
+  const size_t q = align_up(sizeof(float) * static_cast<size_t>(rows) * d_head, 256);
+  const size_t part = align_up(sizeof(float) * static_cast<size_t>(rows) * kRouterChunksMax *
+                                   (LYNX_MAX_FUSED_ROUTER + 1), 256);
+  return q + part + sizeof(int) * static_cast<size_t>(rows) + 512;
 }
 
 int lynx_attention(const lynx_attention_t* attn, const uint16_t* h_in, int B, int Tn, int norm_input,
@@ -638,6 +656,23 @@ int lynx_attention(const lynx_attention_t* attn, const uint16_t* h_in, int B, in
   a.max_len = attn->max_len;
   a.norm_input = norm_input ? 1 : 0;
   a.h_out = h_out;
+  a.router_wt = attn->router_wt;
+  a.N = attn->num_experts;
+  a.logits = attn->logits;
+  a.rpart = nullptr;
+  a.row_arrivals = nullptr;
+  if (attn->router_wt) {
+    if (!attn->logits || attn->num_experts < 1) return LYNX_ERR_SHAPE;
+    if (attn->num_experts > LYNX_MAX_FUSED_ROUTER || attn->d_model > kRouterChunksMax * 1024)
+      return LYNX_ERR_UNSUPPORTED;
+    const int rows = B * Tn;
+    char* base = static_cast<char*>(aligned_ws(workspace));
+    const size_t q = align_up(sizeof(float) * static_cast<size_t>(rows) * attn->d_head, 256);
+    const size_t part = align_up(sizeof(float) * static_cast<size_t>(rows) * kRouterChunksMax *
+                                     (LYNX_MAX_FUSED_ROUTER + 1), 256);
+    a.rpart = reinterpret_cast<float*>(base + q);
+    a.row_arrivals = reinterpret_cast<int*>(base + q + part);
+  }
   return cuda_status(launch_attention(a, stream));
 }
 

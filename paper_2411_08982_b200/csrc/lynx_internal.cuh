@@ -135,6 +135,13 @@ struct AttnArgs {
   const int32_t* pos;
   int B, Tn, d, dh, max_len, norm_input;
   uint16_t* h_out;
+  // fused router (router_wt != null): per-(row, column chunk) partial dots
+  // and sum of squares, the row's last chunk finishes the logits
+  const uint16_t* router_wt;
+  int N;
+  double* logits;
+  float* rpart;       // [B*Tn, chunks, N + 1]
+  int* row_arrivals;  // [B*Tn], zero; re-armed by the last chunk
 };
 size_t attn_out_smem(int d, int dh, int max_len);
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);

@@ -122,20 +122,30 @@ class DecodeStack:
         self.k_cache = torch.zeros((self.L, self.B, self.max_len, attn.d_head), dtype=torch.float32, device=dev)
         self.v_cache = torch.zeros_like(self.k_cache)
         self.pos = torch.zeros((1,), dtype=torch.int32, device=dev)
-        self._attn = []
+        # Decode steps fuse the next MoE layer's router into the attention
+        # output kernel: logits come out with h, K0 drops out.
+        self.fused_router = (s.num_experts <= nat.MAX_FUSED_ROUTER and self.d <= 8192 and
+                             all(r is not None for r in moe.router_wt))
+        self.logits = torch.empty((self.B, s.num_experts), dtype=torch.float64, device=dev)
+        self._attn, self._attn_dec = [], []
         for l in range(self.L):
-            a = nat.LynxAttention()
-            a.d_model, a.d_head, a.max_len = self.d, attn.d_head, self.max_len
-            a.wqkv, a.wo = nat.ptr(attn.wqkv[l]), nat.ptr(attn.wo[l])
-            a.k_cache, a.v_cache = nat.ptr(self.k_cache[l]), nat.ptr(self.v_cache[l])
-            self._attn.append(a)
+            for fused, lst in ((False, self._attn), (self.fused_router, self._attn_dec)):
+                a = nat.LynxAttention()
+                a.d_model, a.d_head, a.max_len = self.d, attn.d_head, self.max_len
+                a.wqkv, a.wo = nat.ptr(attn.wqkv[l]), nat.ptr(attn.wo[l])
+                a.k_cache, a.v_cache = nat.ptr(self.k_cache[l]), nat.ptr(self.v_cache[l])
+                if fused:
+                    a.num_experts, a.router_wt, a.logits = s.num_experts, nat.ptr(moe.router_wt[l]), nat.ptr(self.logits)
+                lst.append(a)
         self._attn_refs = [ctypes_ref(a) for a in self._attn]
+        self._attn_dec_refs = [ctypes_ref(a) for a in self._attn_dec]
         # one MoE workspace shared by every layer (they run in stream order)
         self._decode_layers = self._make_layers(self.B, Phase.DECODE)
         self.prev = torch.zeros((self.B, self.d), dtype=torch.bfloat16, device=dev)
         self._mid = torch.empty_like(self.prev)
         self._alt = [torch.empty_like(self.prev), torch.empty_like(self.prev)]
-        self._attn_ws = torch.empty((int(nat.lib().lynx_attention_workspace_bytes(self.B, attn.d_head)),),
+        # zeroed: holds the fused router's per-row arrival counters (kernel re-arms them)
+        self._attn_ws = torch.zeros((int(nat.lib().lynx_attention_workspace_bytes(self.B, attn.d_head)),),
                                     dtype=torch.uint8, device=dev)
         self._graph = None
         self.steps_done = 0
@@ -158,9 +168,10 @@ class DecodeStack:
         torch.cuda.synchronize()
         return layers
 
-    def _attention(self, l: int, h_in, T_new: int, norm_input: bool, h_out, ws):
+    def _attention(self, l: int, h_in, T_new: int, norm_input: bool, h_out, ws, fused: bool = False):
         torch = _torch()
-        st = nat.lib().lynx_attention(self._attn_refs[l], h_in.data_ptr(), self.B, T_new, 1 if norm_input else 0,
+        ref = self._attn_dec_refs[l] if fused else self._attn_refs[l]
+        st = nat.lib().lynx_attention(ref, h_in.data_ptr(), self.B, T_new, 1 if norm_input else 0,
                                       self.pos.data_ptr(), h_out.data_ptr(), ws.data_ptr(), ws.numel(),
                                       torch.cuda.current_stream().cuda_stream)
         nat.check(st, "lynx_attention")
@@ -207,11 +218,11 @@ class DecodeStack:
     def _step_body(self):
         h = self.prev
         for l in range(self.L):
-            self._attention(l, h, 1, l == 0, self._mid, self._attn_ws)
+            self._attention(l, h, 1, l == 0, self._mid, self._attn_ws, fused=self.fused_router)
             dst = self.prev if l == self.L - 1 else self._alt[l % 2]
             if self.probe is not None:
                 h_in = h.clone()
-            self._decode_layers[l](self._mid, dst)
+            self._decode_layers[l](self._mid, dst, logits=self.logits if self.fused_router else None)
             if self.probe is not None:
                 self.probe(l, Phase.DECODE, h_in, self._mid, dst, self._decode_layers[l])
             if self.trace is not None:
@@ -266,7 +277,7 @@ class DecodeStack:
             a0, a1 = ev(), ev()
             k = [ev() for _ in range(6)]
             a0.record()
-            self._attention(l, h, 1, l == 0, self._mid, self._attn_ws)
+            self._attention(l, h, 1, l == 0, self._mid, self._attn_ws)  # unfused: K0 timed as routing
             a1.record()
             dst = self.prev if l == self.L - 1 else self._alt[l % 2]
             self._decode_layers[l].profiled(self._mid, k, dst)

@@ -285,7 +285,9 @@ class LynxMoELayer:
         self._layer_ref = ctypes_ref(self._layer)
         self._pol_ref = ctypes_ref(self._pol) if self._pol is not None else None
 
-    def __call__(self, hidden, out=None):
+    def __call__(self, hidden, out=None, logits=None):
+        """The layer on device-resident ``hidden`` [T, d] bf16.  ``logits``
+        (f64 [T, N], e.g. from the decode stack's fused router) skips K0."""
         torch = _torch()
         if hidden.dtype != torch.bfloat16 or not hidden.is_cuda or tuple(hidden.shape) != (
                 self.T, self.model.spec.d_model):
@@ -293,10 +295,17 @@ class LynxMoELayer:
                                   f"{self.model.spec.d_model}]")
         if out is None:
             out = torch.empty_like(hidden)
-        st = self._lib.lynx_moe_layer(self._layer_ref, hidden.data_ptr(), self.T,
-                                      1 if self.phase is Phase.DECODE else 0, self._pol_ref, out.data_ptr(),
-                                      self._sel_ref, self.workspace.data_ptr(), self.workspace.numel(),
-                                      torch.cuda.current_stream().cuda_stream)
+        decode = 1 if self.phase is Phase.DECODE else 0
+        stream = torch.cuda.current_stream().cuda_stream
+        if logits is not None:
+            st = self._lib.lynx_moe_layer_logits(self._layer_ref, hidden.data_ptr(), logits.data_ptr(), self.T,
+                                                 decode, self._pol_ref, out.data_ptr(), self._sel_ref,
+                                                 self.workspace.data_ptr(), self.workspace.numel(), stream)
+            nat.check(st, "lynx_moe_layer_logits")
+            return out
+        st = self._lib.lynx_moe_layer(self._layer_ref, hidden.data_ptr(), self.T, decode, self._pol_ref,
+                                      out.data_ptr(), self._sel_ref, self.workspace.data_ptr(),
+                                      self.workspace.numel(), stream)
         nat.check(st, "lynx_moe_layer")
         return out
 

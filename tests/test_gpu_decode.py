@@ -86,16 +86,19 @@ def test_decode_stack_teacher_forced_vs_oracle():
     seen = []
 
     def probe(l, phase, h_in, mid, out, layer):
+        fused = phase is L.Phase.DECODE and stack.fused_router
         seen.append((l, phase, h_in.clone(), mid.clone(), out.clone(), layer.mask(),
                      layer.expert_ids.clone(), int(stack.pos.item()),
-                     stack.k_cache[l].clone(), stack.v_cache[l].clone()))
+                     stack.k_cache[l].clone(), stack.v_cache[l].clone(),
+                     stack.logits.clone() if fused else None))
 
     spec, moe, attn, stack = _stack(policy=pol, probe=probe)
     B, P, d = 4, 3, spec.d_model
     x = np.random.default_rng(0).normal(size=(B, P, d))
     stack.simulate(x, 3)
     assert len(seen) == spec.num_layers * 4
-    for l, phase, h_in, mid, out, mask, ids, pos, kc, vc in seen:
+    assert stack.fused_router
+    for l, phase, h_in, mid, out, mask, ids, pos, kc, vc, fused_logits in seen:
         decode = phase is L.Phase.DECODE
         Tn = 1 if decode else P
         xin = f64(h_in).reshape(B, Tn, d)
@@ -104,8 +107,14 @@ def test_decode_stack_teacher_forced_vs_oracle():
         ref_a, keys, vals = O.attention(xin, *attn_host(attn, l), f64(kc[:, :pos]), f64(vc[:, :pos]), pos)
         assert O.norm_rel_err(f64(mid).reshape(B, Tn, d), xin + ref_a) <= TOL, (l, phase)
         assert np.allclose(f64(kc[:, :pos + Tn]), keys, rtol=1e-3, atol=1e-4), (l, phase)
-        # routing on the kernel's logits: bit-exact decisions
-        logits = f64(L.router_logits(moe, l, mid))
+        # routing on the kernel's logits (decode: the router fused into the
+        # attention kernel; prefill: K0): bit-exact decisions
+        k0_logits = f64(L.router_logits(moe, l, mid))
+        if fused_logits is not None:
+            logits = f64(fused_logits)
+            assert np.allclose(logits, k0_logits, rtol=1e-5, atol=1e-5), (l, phase)
+        else:
+            logits = k0_logits
         r_ids, r_probs, r_full = O.route(logits, spec.top_k)
         opol = O.Policy(mode="latency", drop_count=3)
         ref_mask = O.apply(r_ids, r_probs, r_full, opol, decode=decode)
