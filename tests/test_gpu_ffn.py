@@ -320,3 +320,54 @@ def test_forward_rejects_token_mismatch():
     model = _embed_model(np.stack([np.eye(2), np.eye(2)]), np.stack([np.eye(2), np.eye(2)]), 2, 1)
     with pytest.raises(L.ValidationError):
         L.forward_layer(_hid([[1.0, 0.0], [0.0, 1.0]]), model, 0, _mask([[0]], [[1.0]], 2))
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_layer_configs_vs_oracle(seed):
+    """Randomised whole-layer parity (lynx_moe_layer: K0..K4) over shapes and
+    policies: T 1..300, N 2..64, k 1..min(8,N), shared 0..2, d / ff multiples
+    of 8 (including ones that are not multiples of 64), latency / accuracy
+    policies with random settings, decode and prefill.  Selection bit-exact
+    vs the oracle on the kernel's logits; output within the bf16 tolerance."""
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.choice([2, 3, 5, 8, 12, 16, 24, 33, 48, 64]))
+    k = int(rng.integers(1, min(8, N) + 1))
+    S = int(rng.choice([0, 0, 1, 2]))
+    T = int(rng.choice([1, 3, 16, 31, 64, 100, 257, 300]))
+    d = int(rng.choice([64, 136, 256, 512]))
+    ff = int(rng.choice([64, 120, 192, 512]))
+    decode = bool(rng.integers(0, 4))  # mostly decode
+    if rng.integers(0, 2):
+        cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 1)))
+        opol = O.Policy(mode="latency", drop_count=cfg.drop_count)
+    else:
+        mk = int(rng.integers(k, N + 1)) if rng.integers(0, 2) else None
+        cfg = L.PolicyConfig(mode="accuracy", confidence_threshold=float(rng.choice([0.2, 0.4, 0.6])),
+                             sample_threshold=int(rng.integers(1, 12)), min_experts=mk,
+                             freq_keep_budget=int(rng.integers(1, N + 1)),
+                             confidence_metric=str(rng.choice(["top1", "margin"])))
+        opol = O.Policy(mode="accuracy", confidence_threshold=cfg.confidence_threshold,
+                        sample_threshold=cfg.sample_threshold, min_experts=mk,
+                        freq_keep_budget=cfg.freq_keep_budget, confidence_metric=cfg.confidence_metric)
+    spec = L.MoEModelSpec(1, N, k, d, ff, num_shared_experts=S)
+    model = L.build_swiglu_model(spec, seed=seed)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    hidden = torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16)
+    layer = L.LynxMoELayer(model, 0, T, policy=cfg, phase=L.Phase.DECODE if decode else L.Phase.PREFILL)
+    y = layer(hidden)
+    torch.cuda.synchronize()
+    logits = _np(L.router_logits(model, 0, hidden))
+    ids, probs, full = O.route(logits, k)
+    ref_mask = O.apply(ids, probs, full, opol, decode=decode)
+    tag = dict(N=N, k=k, S=S, T=T, d=d, ff=ff, decode=decode, cfg=cfg)
+    assert np.array_equal(_np(layer.expert_ids), ids), tag
+    assert np.array_equal(_np(layer.assigned), ref_mask.assigned), tag
+    keep = np.zeros(N, dtype=np.uint8)
+    keep[ref_mask.retained] = 1
+    assert np.array_equal(_np(layer.retained_mask), keep), tag
+    assert np.allclose(_np(layer.weights), ref_mask.weights, rtol=1e-12, atol=1e-15), tag
+    w1, w3 = L.unpack_w13(model.w13[0], ff)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights,
+                           round_h_bf16=True, shared=range(N, N + S))
+    assert O.norm_rel_err(_np(y), ref) <= TOL, tag
