@@ -18,10 +18,10 @@
 //   dispatch order             simulator.py:104-112
 //
 // These kernels are latency-bound (a decode batch is a few KB of routing
-// state): K1 is one CTA, one warp per token with lanes over experts, every
-// per-token array staged in shared memory, and compact (non-inlined) code --
-// the kernel runs once per layer from a cold instruction cache, so code
-// size is latency.
+// state): K1 is one CTA -- a thread per token for N <= 16 (route_select_fast),
+// eight lanes per token otherwise (route_select_group) -- with every
+// per-token array staged in shared memory when it fits, and rolled loops:
+// the kernel runs once per layer from a cold instruction cache.
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -74,27 +74,6 @@ __device__ __noinline__ double np_pairwise_sum(const double* a, int n) {
   return np_pairwise_sum(a, half) + np_pairwise_sum(a + half, n - half);
 }
 
-// Same sum computed by a warp: lanes 0..7 each run one strided partial in
-// numpy's order; lane 0 folds.  Result broadcast to all lanes.
-__device__ __noinline__ double warp_pairwise_sum(const double* a, int n) {
-  const int lane = threadIdx.x & 31;
-  if (n < 8 || n > 128) {
-    double acc = lane == 0 ? np_pairwise_sum(a, n) : 0.0;
-    return __shfl_sync(kFull, acc, 0);
-  }
-  const int body = n - (n % 8);
-  double r = 0.0;
-  if (lane < 8) {
-    r = a[lane];
-    for (int i = 8 + lane; i < body; i += 8) r += a[i];
-  }
-  double part[8];
-  for (int j = 0; j < 8; ++j) part[j] = __shfl_sync(kFull, r, j);
-  double acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
-  for (int i = body; i < n; ++i) acc += a[i];
-  return acc;  // identical on every lane
-}
-
 __device__ __forceinline__ uint64_t expert_mask_all(int N) { return N == 64 ? ~0ull : ((1ull << N) - 1); }
 
 // Warp argmax over the experts in `cand` by (value desc, index asc); each
@@ -128,62 +107,6 @@ __device__ __forceinline__ double lane_value(double v0, double v1, int e) {
   const double a = __shfl_sync(kFull, v0, e & 31);
   const double b = __shfl_sync(kFull, v1, e & 31);
   return e < 32 ? a : b;
-}
-
-// Softmax + stable top-k + confidence for one token (router.py:141-187,
-// 125-138).  With z == null the row p and ids/probs are inputs.
-__device__ __noinline__ void route_token(const double* z, double* p, int N, int k, int metric, int32_t* ids,
-                                         double* probs, double* conf, int* flags) {
-  const int lane = threadIdx.x & 31;
-  const int e0 = lane, e1 = lane + 32;
-  const uint64_t all = expert_mask_all(N);
-  double v0 = 0.0, v1 = 0.0;
-  if (z) {
-    const double z0 = e0 < N ? z[e0] : 0.0, z1 = e1 < N ? z[e1] : 0.0;
-    const bool bad = (e0 < N && !isfinite(z0)) || (e1 < N && !isfinite(z1));
-    if (__any_sync(kFull, bad) && lane == 0) atomicOr(flags, LYNX_FLAG_NONFINITE);
-    double m = e0 < N ? z0 : -INFINITY;
-    if (e1 < N && z1 > m) m = z1;
-    for (int off = 16; off > 0; off >>= 1) {
-      const double o = __shfl_xor_sync(kFull, m, off);
-      m = o > m ? o : m;
-    }
-    if (e0 < N) p[e0] = exp(z0 - m);
-    if (e1 < N) p[e1] = exp(z1 - m);
-    __syncwarp();
-    const double s = warp_pairwise_sum(p, N);
-    if (e0 < N) p[e0] = p[e0] / s;
-    if (e1 < N) p[e1] = p[e1] / s;
-    __syncwarp();
-  }
-  v0 = e0 < N ? p[e0] : 0.0;
-  v1 = e1 < N ? p[e1] : 0.0;
-  if (z) {
-    uint64_t taken = 0;
-    for (int r = 0; r < k; ++r) {
-      double bv;
-      const int b = warp_best(v0, v1, all & ~taken, &bv);
-      taken |= 1ull << b;
-      if (lane == 0) {
-        ids[r] = b;
-        probs[r] = bv;
-      }
-    }
-  }
-  double top1;
-  const int first = warp_best(v0, v1, all, &top1);
-  double c = top1;
-  if (metric == LYNX_CONF_MARGIN) {
-    if (N == 1) {
-      c = v0;  // lane 0 holds p[0]
-      c = __shfl_sync(kFull, c, 0);
-    } else {  // np.sort(full)[-1] - np.sort(full)[-2]
-      double second;
-      warp_best(v0, v1, all & ~(1ull << first), &second);
-      c = top1 - second;
-    }
-  }
-  if (lane == 0) *conf = c;
 }
 
 // remap_tokens for one token (policy.py:171-210), one warp.
@@ -605,124 +528,6 @@ __device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* ID
       if (lane == 0) *s_clipped = need > 0;
     }
   }
-}
-
-// ------------------------------------------------------------------- K1
-__global__ void __launch_bounds__(kSelectThreads) route_select_kernel(const __grid_constant__ SelectArgs a) {
-  __shared__ double s_counts[LYNX_MAX_EXPERTS];
-  __shared__ int s_icount[LYNX_MAX_EXPERTS];
-  __shared__ int s_rank[LYNX_MAX_EXPERTS];
-  __shared__ int s_order[LYNX_MAX_EXPERTS];
-  __shared__ int s_keep[LYNX_MAX_EXPERTS];
-  __shared__ int s_flags, s_nq, s_clipped;
-  __shared__ unsigned long long s_keepmask;
-  extern __shared__ __align__(16) uint8_t s_dyn[];
-
-  griddep_launch_dependents();
-  const int T = a.T, N = a.N, k = a.k;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
-  const SelectSmem L = select_smem(T, N, k, a.stage, a.plan.enabled);
-  // Working arrays: shared memory when they fit, else the caller's outputs.
-  double* P = a.stage ? reinterpret_cast<double*>(s_dyn + L.p) : a.full;
-  double* CONF = a.stage ? reinterpret_cast<double*>(s_dyn + L.conf) : a.conf;
-  int32_t* IDS = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.ids) : a.ids;
-  double* PROBS = a.stage ? reinterpret_cast<double*>(s_dyn + L.probs) : a.probs;
-  int32_t* ASG = a.stage ? reinterpret_cast<int32_t*>(s_dyn + L.asg) : a.assigned;
-  double* WT = a.stage ? reinterpret_cast<double*>(s_dyn + L.w) : a.weights;
-  uint8_t* IMP = s_dyn + L.imp;
-
-  if (tid == 0) {
-    s_flags = 0;
-    s_nq = 0;
-    s_clipped = 0;
-  }
-  for (int e = tid; e < N; e += nthr) s_icount[e] = 0;
-  SEL_TS(0);
-  griddep_wait();  // logits come from K0 (programmatic dependent launch)
-  if (!a.logits && a.stage) {  // apply_policy on a given selection: stage it
-    for (int i = tid; i < T * N; i += nthr) P[i] = a.full[i];
-    for (int i = tid; i < T * k; i += nthr) {
-      IDS[i] = a.ids[i];
-      PROBS[i] = a.probs[i];
-    }
-  }
-  __syncthreads();
-
-  SEL_TS(1);
-  // 1) softmax + top-k + confidence: one warp per token
-  for (int t = warp; t < T; t += nwarps)
-    route_token(a.logits ? a.logits + static_cast<size_t>(t) * N : nullptr, P + static_cast<size_t>(t) * N, N, k,
-                a.pol.confidence_metric, IDS + t * k, PROBS + t * k, CONF + t, &s_flags);
-  __syncthreads();
-
-  SEL_TS(2);
-  const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
-  const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
-  if (!run_policy) {  // full_retain_mask: identity, weights = probs / row sum
-    for (int t = tid; t < T; t += nthr) {
-      const double s = np_pairwise_sum(PROBS + t * k, k);
-      for (int r = 0; r < k; ++r) {
-        ASG[t * k + r] = IDS[t * k + r];
-        WT[t * k + r] = PROBS[t * k + r] / s;
-      }
-      IMP[t] = 0;
-    }
-    for (int e = tid; e < N; e += nthr) {
-      s_keep[e] = 1;
-      s_counts[e] = 0.0;
-    }
-  } else {
-    batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long m = 0;
-    for (int e = 0; e < N; ++e)
-      if (s_keep[e]) m |= 1ull << e;
-    s_keepmask = m;
-  }
-  __syncthreads();
-
-  SEL_TS(3);
-  // 2) remap every token onto the retained set: one warp per token
-  if (run_policy) {
-    const uint64_t keep = s_keepmask;
-    for (int t = warp; t < T; t += nwarps)
-      remap_token(IDS + t * k, P + static_cast<size_t>(t) * N, k, N, keep, ASG + t * k, WT + t * k, &s_flags);
-  }
-  __syncthreads();
-
-  SEL_TS(4);
-  // 3) outputs
-  if (a.stage) {
-    if (a.logits) {
-      for (int i = tid; i < T * N; i += nthr) a.full[i] = P[i];
-      for (int i = tid; i < T * k; i += nthr) {
-        a.ids[i] = IDS[i];
-        a.probs[i] = PROBS[i];
-      }
-    }
-    for (int t = tid; t < T; t += nthr) a.conf[t] = CONF[t];
-    for (int i = tid; i < T * k; i += nthr) {
-      a.assigned[i] = ASG[i];
-      a.weights[i] = WT[i];
-    }
-  }
-  for (int e = tid; e < N; e += nthr) {
-    if (a.retained) a.retained[e] = static_cast<uint8_t>(s_keep[e]);
-    if (a.counts) a.counts[e] = s_counts[e];
-  }
-  if (a.important)
-    for (int t = tid; t < T; t += nthr) a.important[t] = accuracy ? IMP[t] : 0;
-  if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
-
-  SEL_TS(5);
-  // 4) dispatch plan for K2/K3 (layer path)
-  if (a.plan.enabled)
-    plan_dispatch(ASG, WT, T, N, k, a.plan, reinterpret_cast<uint32_t*>(s_dyn + L.bits),
-                  reinterpret_cast<int*>(s_dyn + L.prefix));
-  SEL_TS(6);
 }
 
 // ------------------------------------------------- K1 fast path (N <= 16)
@@ -1422,25 +1227,9 @@ static cudaError_t allow_big_smem(const void* fn, int& configured_device) {
   return e;
 }
 
-// LYNX_SELECT_WARP=1 forces the warp-per-token kernel for N > 16 (A/B and
-// cross-check of the group path).
-static bool group_path_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LYNX_SELECT_WARP");
-    v = (e && atoi(e)) ? 0 : 1;
-  }
-  return v == 1;
-}
-
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
   const size_t smem = select_smem_bytes(a.T, a.N, a.k, a.stage, a.plan.enabled);
   if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
-  static int configured = -1;
-  if (smem > 48 * 1024) {
-    cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_kernel), configured);
-    if (e != cudaSuccess) return e;
-  }
   // Fast path: N <= 16 and one thread per token (the decode case).
   if (a.N <= 16 && a.T <= kSelectThreads && a.stage) {
     const int threads = ((a.T > a.N ? a.T : a.N) + 31) / 32 * 32;
@@ -1458,23 +1247,21 @@ cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
     }
     return launch_pdl(route_select_fast<16>, dim3(1), dim3(threads), smem, s, a);
   }
-  // Group path: 16 < N <= 64, eight lanes per token.
-  if (group_path_enabled()) {
-    static int configured32 = -1, configured64 = -1;
-    if (a.N <= 32) {
-      if (smem > 48 * 1024) {
-        cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<4>), configured32);
-        if (e != cudaSuccess) return e;
-      }
-      return launch_pdl(route_select_group<4>, dim3(1), dim3(kSelectThreads), smem, s, a);
-    }
+  // Group path: every other shape (N <= 64, or rows too large to stage),
+  // eight lanes per token.
+  static int configured32 = -1, configured64 = -1;
+  if (a.N <= 32) {
     if (smem > 48 * 1024) {
-      cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<8>), configured64);
+      cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<4>), configured32);
       if (e != cudaSuccess) return e;
     }
-    return launch_pdl(route_select_group<8>, dim3(1), dim3(kSelectThreads), smem, s, a);
+    return launch_pdl(route_select_group<4>, dim3(1), dim3(kSelectThreads), smem, s, a);
   }
-  return launch_pdl(route_select_kernel, dim3(1), dim3(kSelectThreads), smem, s, a);
+  if (smem > 48 * 1024) {
+    cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<8>), configured64);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_pdl(route_select_group<8>, dim3(1), dim3(kSelectThreads), smem, s, a);
 }
 
 cudaError_t launch_plan(const int32_t* asg, const double* w, int T, int N, int k, const PlanOut& o, cudaStream_t s) {
