@@ -54,12 +54,11 @@ def main():
     base = t0.min()
     used = layer.used_experts()
     nrows = int(((torch.bincount(layer.assigned.flatten().long(), minlength=N) + 15) // 16 * 16).sum().item())
-    nseg = int(layer.workspace.new_tensor([0]).numel())  # placeholder (segments = used experts here)
-    # unit classes (queue order: gather rows, phase-0, phase-1)
+    # unit classes (queue order: phase-0 units, then phase-1 units)
     tiles1 = 2 * ((ff + 63) // 64) * 64 // 128
-    ngather = nrows if os.environ.get("LYNX_FUSED_GATHER", "0") == "1" else 0
+    ngather = 0
     nA = used * tiles1
-    out = {"records": int(n), "kernel_span_us": float((t1.max() - base) / 1e3), "ngather": ngather, "nA": nA}
+    out = {"records": int(n), "kernel_span_us": float((t1.max() - base) / 1e3), "nA": nA}
     m = role == 4
     dur = (t1[m] - t0[m]) / 1e3
     u = uid[m]
