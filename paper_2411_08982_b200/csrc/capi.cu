@@ -254,7 +254,12 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   const Geometry g = geometry(L, T);
   const PlanOut o = plan_out(ws, P, S);
 
-  GatherArgs ga;
+  GatherArgs ga{};
+  if (peers) {
+    ga.ep.enabled = 1;
+    ga.ep.kind = kSigDispatch;
+    ga.ep.P = *peers;
+  }
   ga.hidden = hidden;
   ga.perm_token = o.perm_token;
   ga.n_rows = o.n_rows;
@@ -718,11 +723,12 @@ int lynx_ep_p2p_route(const uint16_t* router_wt, const uint16_t* hidden_local, i
   if (!router_wt || !hidden_local || d < 8 || N < 1 || N % peers->world_size) return LYNX_ERR_SHAPE;
   if (d % 8 || N > LYNX_MAX_EXPERTS || peers->world_size * peers->tokens_per_rank > LYNX_MAX_TOKENS)
     return LYNX_ERR_UNSUPPORTED;
-  const int Tl = peers->tokens_per_rank;
-  st = cuda_status(launch_router_logits(hidden_local, router_wt, Tl, d, N,
-                                        peers->logits_local + static_cast<size_t>(peers->rank) * Tl * N, stream));
-  if (st) return st;
-  return cuda_status(launch_ep_put_logits(*peers, N, stream));
+  // K0 stores this rank's logits rows into every rank's buffer and signals
+  EpLink put{};
+  put.enabled = 1;
+  put.P = *peers;
+  return cuda_status(launch_router_logits(hidden_local, router_wt, peers->tokens_per_rank, d, N,
+                                          peers->logits_local, stream, &put));
 }
 
 int lynx_ep_p2p_dispatch(const uint16_t* hidden_local, int N, int k, int d, int decode, const lynx_policy_t* policy,
@@ -739,9 +745,10 @@ int lynx_ep_p2p_dispatch(const uint16_t* hidden_local, int N, int k, int d, int 
   int floor_keep = k;
   st = check_policy(policy, k, decode, &floor_keep);
   if (st) return st;
-  st = cuda_status(launch_ep_wait(*peers, kSigLogits, stream));
-  if (st) return st;
   SelectArgs a = select_args(peers->logits_local, T, N, k, decode, policy, floor_keep);
+  a.ep.enabled = 1;  // K1 waits for every rank's logits itself
+  a.ep.kind = kSigLogits;
+  a.ep.P = *peers;
   a.ids = sel->expert_ids;
   a.probs = sel->probs;
   a.full = sel->full_probs;
@@ -758,8 +765,7 @@ int lynx_ep_p2p_expert(const lynx_layer_t* local_layer, int N, const int32_t* as
   if (!local_layer || !assigned || !weights || !assigned_local || !weights_local) return LYNX_ERR_SHAPE;
   const int G = peers->world_size, T = G * peers->tokens_per_rank;
   if (N % G || local_layer->num_experts * G != N) return LYNX_ERR_SHAPE;
-  st = cuda_status(launch_ep_wait(*peers, kSigDispatch, stream));
-  if (st) return st;
+  // the gather kernel (K2) waits for every rank's rows itself
   st = cuda_status(launch_ep_local_mask(assigned, weights, T, local_layer->top_k, N, G, peers->rank, assigned_local,
                                         weights_local, stream));
   if (st) return st;

@@ -17,9 +17,13 @@ namespace lynx {
 // segments, 16-row padded) that K3's TMA tensor map covers.  One 16-byte
 // vector per thread; padding rows are zero.  The permutation itself was
 // planned by K1 (plan_dispatch in select.cu).
-__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+__global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ GatherArgs a) {
   griddep_launch_dependents();
   griddep_wait();
+  if (a.ep.enabled) {  // peer-memory EP: every rank's dispatched rows have landed
+    if (threadIdx.x == 0) wait_peers(a.ep.P, a.ep.kind, *a.ep.P.epoch + 1);
+    __syncthreads();
+  }
   const int rows = *a.n_rows;
   const int nvec = a.d >> 3;
   const uint4* src = reinterpret_cast<const uint4*>(a.hidden);

@@ -1,9 +1,11 @@
 // ep_p2p.cu -- expert parallelism over NVLink peer memory:
 // the logits all-gather, the token dispatch and the partial-sum return are
 // plain stores into the peers' symmetric buffers issued by the kernels that
-// produce the data, each followed by one release-signal per peer; the
-// consumer kernels acquire-wait on those signals.  No NCCL call, no staging
-// copy: the "collective" is fused into the producing kernel.
+// produce the data (K0, the dispatch kernel, K4), each followed by one
+// release-signal per peer; the consuming kernels (K1, K2, the combine)
+// acquire-wait on those signals at their start.  No NCCL call, no staging
+// copy, no extra launch: the "collective" is fused into the producer and
+// consumer kernels.
 //
 // Buffers (identical layout on every rank, peers reach them through the
 // pointer arrays of lynx_ep_peers_t):
@@ -21,32 +23,8 @@
 
 namespace lynx {
 
-// ---------------------------------------------------------------- route
-// This rank's logits rows (already in its own logits buffer at rows
-// rank*Tl..) copied into every peer's buffer, then signalled.
-__global__ void ep_put_logits_kernel(const __grid_constant__ lynx_ep_peers_t P, int N) {
-  griddep_launch_dependents();
-  griddep_wait();
-  const int epoch = *P.epoch + 1;
-  const size_t off = static_cast<size_t>(P.rank) * P.tokens_per_rank * N;
-  const int n = P.tokens_per_rank * N;
-  const double* src = P.logits_local + off;
-  for (int p = 0; p < P.world_size; ++p) {
-    if (p == P.rank) continue;
-    double* dst = P.logits[p] + off;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) signal_peers(P, kSigLogits, epoch);
-}
-
-// One thread waits for `kind` from every peer; the stream's next kernels
-// then read the data.
-__global__ void ep_wait_kernel(const __grid_constant__ lynx_ep_peers_t P, int kind) {
-  griddep_launch_dependents();
-  griddep_wait();
-  if (threadIdx.x == 0) wait_peers(P, kind, *P.epoch + 1);
-}
+// route: K0 itself stores its logits rows into every rank and signals
+// (router_logits_kernel with an EpLink); K1 waits for them at its start.
 
 // ------------------------------------------------------------- dispatch
 // Row i of this rank goes to peer p's recv buffer (rows rank*Tl + i) iff
@@ -108,12 +86,6 @@ __global__ void __launch_bounds__(256) ep_p2p_combine_kernel(const __grid_consta
   }
 }
 
-cudaError_t launch_ep_put_logits(const lynx_ep_peers_t& P, int N, cudaStream_t s) {
-  return launch_pdl(ep_put_logits_kernel, dim3(1), dim3(256), 0, s, P, N);
-}
-cudaError_t launch_ep_wait(const lynx_ep_peers_t& P, int kind, cudaStream_t s) {
-  return launch_pdl(ep_wait_kernel, dim3(1), dim3(32), 0, s, P, kind);
-}
 cudaError_t launch_ep_dispatch(const lynx_ep_peers_t& P, const uint16_t* hidden_local, const int32_t* assigned, int k,
                                int N, int d, cudaStream_t s) {
   return launch_pdl(ep_dispatch_kernel, dim3(P.tokens_per_rank, P.world_size), dim3(128), 0, s, P, hidden_local,

@@ -43,6 +43,15 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Peer-memory EP hooks inside the layer kernels (ep_p2p.cu): K0 stores its
+// logits rows into every peer and signals; K1 / K2 wait for every peer's
+// logits / rows before reading them.  enabled = 0: plain single-GPU kernels.
+struct EpLink {
+  int enabled;
+  int kind;  // the signal this kernel waits for (K1: logits, K2: dispatch)
+  lynx_ep_peers_t P;
+};
+
 // Dispatch plan written by K1 (or the standalone plan kernel).
 struct PlanOut {
   int enabled;
@@ -79,6 +88,7 @@ struct SelectArgs {
   uint8_t* important;
   int32_t* flags;
   PlanOut plan;
+  EpLink ep;  // peer-memory EP: wait for every peer's logits first
 };
 
 // Grouped expert FFN (K3).  Phase 0 = gate/up (or tanh w1) over d, phase 1 =
@@ -122,6 +132,7 @@ struct GatherArgs {
   const int32_t* n_rows;
   int rows_cap, d;
   uint16_t* x_perm;
+  EpLink ep;  // peer-memory EP: wait for every peer's dispatched rows first
 };
 
 // Attention stand-in (attention.cu).
@@ -150,15 +161,13 @@ cudaError_t launch_advance_position(int32_t* pos, int by, cudaStream_t s);
 cudaError_t launch_trace_append(const lynx_trace_ring_t& r, const int32_t* pos, int layer,
                                 const lynx_selection_t& sel, cudaStream_t s);
 
-cudaError_t launch_ep_put_logits(const lynx_ep_peers_t& P, int N, cudaStream_t s);
-cudaError_t launch_ep_wait(const lynx_ep_peers_t& P, int kind, cudaStream_t s);
 cudaError_t launch_ep_dispatch(const lynx_ep_peers_t& P, const uint16_t* hidden_local, const int32_t* assigned, int k,
                                int N, int d, cudaStream_t s);
 cudaError_t launch_ep_p2p_combine(const lynx_ep_peers_t& P, const uint16_t* hidden_local, int d, uint16_t* out,
                                   cudaStream_t s);
 
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
-                                 cudaStream_t s);
+                                 cudaStream_t s, const EpLink* put = nullptr);
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan);
 bool select_can_stage(int T, int N, int k, bool plan);
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s);

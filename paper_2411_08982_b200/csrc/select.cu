@@ -27,6 +27,7 @@
 #include <stdlib.h>
 
 #include "lynx_internal.cuh"
+#include "p2p.cuh"
 #include "ptx.cuh"
 
 namespace lynx {
@@ -612,6 +613,10 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
   if (t < N) s_icount[t] = 0;
   SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
+  if (a.ep.enabled) {  // peer-memory EP: every rank's logits rows have landed
+    if (threadIdx.x == 0) wait_peers(a.ep.P, a.ep.kind, *a.ep.P.epoch + 1);
+    __syncthreads();
+  }
   SEL_TS(1);
 
   // 1) softmax + stable top-k + confidence, thread per token
@@ -876,6 +881,10 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   if (tid < N) s_icount[tid] = 0;
   SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
+  if (a.ep.enabled) {  // peer-memory EP: every rank's logits rows have landed
+    if (threadIdx.x == 0) wait_peers(a.ep.P, a.ep.kind, *a.ep.P.epoch + 1);
+    __syncthreads();
+  }
   SEL_TS(1);
 
   // 1) softmax + stable top-k + confidence, eight lanes per token.  Passes
@@ -1143,7 +1152,8 @@ __global__ void vote_kernel(const int32_t* ids, int T, int k, int N, lynx_policy
 // 16-byte loads before any math, so an iteration costs one memory latency.
 __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __restrict__ hidden,
                                                             const uint16_t* __restrict__ wt, int d, int N,
-                                                            double* __restrict__ logits) {
+                                                            double* __restrict__ logits,
+                                                            const __grid_constant__ EpLink put) {
   griddep_launch_dependents();
   const int t = blockIdx.x;
   const int n0 = blockIdx.y * 8;
@@ -1199,14 +1209,25 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __re
   __syncthreads();
   if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
     const double inv = 1.0 / sqrt(static_cast<double>(s_red[0][8]) / d + 1e-12);
-    logits[static_cast<size_t>(t) * N + n0 + threadIdx.x] = static_cast<double>(s_red[0][threadIdx.x]) * inv;
+    const double z = static_cast<double>(s_red[0][threadIdx.x]) * inv;
+    if (put.enabled) {  // peer-memory EP: this rank's rows straight into every rank's logits buffer
+      const size_t o = (static_cast<size_t>(put.P.rank) * put.P.tokens_per_rank + t) * N + n0 + threadIdx.x;
+      for (int p = 0; p < put.P.world_size; ++p) put.P.logits[p][o] = z;
+    } else {
+      logits[static_cast<size_t>(t) * N + n0 + threadIdx.x] = z;
+    }
+  }
+  if (put.enabled && last_cta(put.P.counters + 3)) {
+    if (threadIdx.x == 0) signal_peers(put.P, kSigLogits, *put.P.epoch + 1);
   }
 }
 
 // ------------------------------------------------------------- launchers
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
-                                 cudaStream_t s) {
-  return launch_pdl(router_logits_kernel, dim3(T, (N + 7) / 8), dim3(256), 0, s, hidden, wt, d, N, logits);
+                                 cudaStream_t s, const EpLink* put) {
+  EpLink none{};
+  return launch_pdl(router_logits_kernel, dim3(T, (N + 7) / 8), dim3(256), 0, s, hidden, wt, d, N, logits,
+                    put ? *put : none);
 }
 
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan) {
