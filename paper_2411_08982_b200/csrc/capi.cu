@@ -85,6 +85,16 @@ int kb2_per_unit(int kb2_total) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// LYNX_ROUTE_IN_K1=1 keeps the routing in K1 for N > 16 (A/B switch).
+bool route_in_k0_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LYNX_ROUTE_IN_K1");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 struct Caps {
   int max_seg, rows_cap;
 };
@@ -389,7 +399,10 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
 
   const double* logits = given_logits;
   record(ev, 0, stream);
-  if (!logits) {
+  // N > 16: the routing itself runs inside K0 (clusters per token) and K1
+  // takes the selection as given; N <= 16 keeps it in K1's thread-per-token path.
+  const bool route_in_k0 = !logits && N > 16 && route_in_k0_enabled();
+  if (!logits && !route_in_k0) {
     double* lg = at<double>(ws, P.logits);
     st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, lg, stream));
     if (st) return st;
@@ -411,6 +424,11 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   a.flags = LYNX_PICK(flags, flags, int32_t);
 #undef LYNX_PICK
   a.plan = plan_out(ws, P, layer->num_shared);
+  if (route_in_k0) {
+    st = cuda_status(launch_router_route(hidden, layer->router_wt, T, layer->d_model, N, k, nullptr, a.full, a.ids,
+                                         a.probs, stream));
+    if (st) return st;
+  }
   record(ev, 1, stream);
   st = cuda_status(launch_route_select(a, stream));
   if (st) return st;

@@ -168,6 +168,10 @@ cudaError_t launch_ep_p2p_combine(const lynx_ep_peers_t& P, const uint16_t* hidd
 
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s, const EpLink* put = nullptr);
+// K0 + routing for 16 < N <= 64 (clusters of ceil(N/8) CTAs per token):
+// writes full/ids/probs (and logits if non-null); K1 then runs on the given selection.
+cudaError_t launch_router_route(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, int k,
+                                double* logits, double* full, int32_t* ids, double* probs, cudaStream_t s);
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan);
 bool select_can_stage(int T, int N, int k, bool plan);
 cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s);

@@ -22,6 +22,7 @@
 // eight lanes per token otherwise (route_select_group) -- with every
 // per-token array staged in shared memory when it fits, and rolled loops:
 // the kernel runs once per layer from a cold instruction cache.
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -948,6 +949,8 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
         const int e = j + 8 * q;
         v[q] = (live && e < N) ? a.full[static_cast<size_t>(t) * N + e] : 0.0;
         if (live && e < N) P[static_cast<size_t>(t) * N + e] = v[q];
+        // a row routed from non-finite logits arrives as NaN (router_route_kernel)
+        if (live && e < N && isnan(v[q])) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
       }
       if (live && j < k) {
         IDS[t * k + j] = a.ids[t * k + j];
@@ -1150,20 +1153,17 @@ __global__ void vote_kernel(const int32_t* ids, int T, int k, int N, lynx_policy
 // logits[t, n] = (h_t . Wr_n) / sqrt(mean(h_t^2) + 1e-12).  One CTA per
 // (token, group of 8 experts); every thread issues its 1 + 8 independent
 // 16-byte loads before any math, so an iteration costs one memory latency.
-__global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __restrict__ hidden,
-                                                            const uint16_t* __restrict__ wt, int d, int N,
-                                                            double* __restrict__ logits,
-                                                            const __grid_constant__ EpLink put) {
-  griddep_launch_dependents();
-  const int t = blockIdx.x;
-  const int n0 = blockIdx.y * 8;
+// The 8 logits of experts n0..n0+7 for token row h (RMSNorm fused: dots and
+// the row's sum of squares in one pass, f64 result dot / sqrt(ss / d + eps)).
+// 256 threads; result valid in threads 0..7 (z), all threads return.
+__device__ __forceinline__ double router_dots8(const uint16_t* __restrict__ hidden, const uint16_t* __restrict__ wt,
+                                               int t, int d, int N, int n0) {
   const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(hidden) + static_cast<size_t>(t) * d;
   const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(wt);
   float acc[8];
 #pragma unroll
   for (int n = 0; n < 8; ++n) acc[n] = 0.f;
   float ss = 0.f;
-  griddep_wait();  // hidden may be produced by the previous kernel
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
     uint4 wv[8];
     const uint4 hv = *reinterpret_cast<const uint4*>(h + c);
@@ -1207,9 +1207,24 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __re
     s_red[0][threadIdx.x] = v;
   }
   __syncthreads();
-  if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
+  double z = 0.0;
+  if (threadIdx.x < 8) {
     const double inv = 1.0 / sqrt(static_cast<double>(s_red[0][8]) / d + 1e-12);
-    const double z = static_cast<double>(s_red[0][threadIdx.x]) * inv;
+    z = static_cast<double>(s_red[0][threadIdx.x]) * inv;
+  }
+  return z;
+}
+
+__global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __restrict__ hidden,
+                                                            const uint16_t* __restrict__ wt, int d, int N,
+                                                            double* __restrict__ logits,
+                                                            const __grid_constant__ EpLink put) {
+  griddep_launch_dependents();
+  const int t = blockIdx.x;
+  const int n0 = blockIdx.y * 8;
+  griddep_wait();  // hidden may be produced by the previous kernel
+  const double z = router_dots8(hidden, wt, t, d, N, n0);
+  if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
     if (put.enabled) {  // peer-memory EP: this rank's rows straight into every rank's logits buffer
       const size_t o = (static_cast<size_t>(put.P.rank) * put.P.tokens_per_rank + t) * N + n0 + threadIdx.x;
       for (int p = 0; p < put.P.world_size; ++p) put.P.logits[p][o] = z;
@@ -1222,12 +1237,102 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __re
   }
 }
 
+// K0 with the routing folded in (router.py:141-187), for 16 < N <= 64.  A
+// cluster of ceil(N/8) CTAs per token computes the token's logits (8 experts
+// per CTA, router_dots8) into the cluster leader's shared memory (DSMEM);
+// after one cluster barrier the leader's first eight lanes run the group
+// path's softmax (numpy pairwise sum) + stable top-k for the token.  The
+// softmax over 64 experts of 128 tokens then spreads over 128 SMs instead of
+// one (K1 is a single CTA), and K1 runs on the given selection.  Rows with
+// non-finite logits are written as NaN so K1 raises LYNX_FLAG_NONFINITE.
+__global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __restrict__ hidden,
+                                                           const uint16_t* __restrict__ wt, int d, int N, int k,
+                                                           double* logits, double* full, int32_t* ids,
+                                                           double* probs) {
+  namespace cg = cooperative_groups;
+  __shared__ double zs[LYNX_MAX_EXPERTS];
+  cg::cluster_group cluster = cg::this_cluster();
+  griddep_launch_dependents();
+  const int t = blockIdx.y, c = static_cast<int>(cluster.block_rank());
+  const int n0 = c * 8;
+  griddep_wait();  // hidden may be produced by the previous kernel
+  const double z = router_dots8(hidden, wt, t, d, N, n0);
+  if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
+    double* zl = cluster.map_shared_rank(zs, 0);
+    zl[n0 + threadIdx.x] = z;
+    if (logits) logits[static_cast<size_t>(t) * N + n0 + threadIdx.x] = z;
+  }
+  cluster.sync();
+  if (c != 0 || threadIdx.x >= 32) return;
+  // warp 0 of the leader: lanes 0..7 route token t (group 0); the other
+  // groups of the warp shadow it on zeros (shuffles stay warp-converged)
+  const int j = threadIdx.x & 7, gbase = threadIdx.x & 24;
+  const bool live = threadIdx.x < 8;
+  constexpr int EPL = 8;
+  double v[EPL];
+  bool bad = false;
+  double m = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < EPL; ++q) {
+    const int e = j + 8 * q;
+    v[q] = e < N ? (live ? zs[e] : 0.0) : -INFINITY;
+    if (e < N) bad |= !isfinite(v[q]);
+    m = v[q] > m ? v[q] : m;
+  }
+  m = fmax(m, __shfl_xor_sync(kFull, m, 1));
+  m = fmax(m, __shfl_xor_sync(kFull, m, 2));
+  m = fmax(m, __shfl_xor_sync(kFull, m, 4));
+  bad = __any_sync(kFull, live && bad);
+#pragma unroll
+  for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? exp(v[q] - m) : 0.0;
+  const double sum = grp_pairwise<EPL>(v, N, j, gbase);
+#pragma unroll
+  for (int q = 0; q < EPL; ++q) v[q] = v[q] / sum;  // e / s, as numpy divides
+  if (live) {
+#pragma unroll
+    for (int q = 0; q < EPL; ++q)
+      if (j + 8 * q < N) full[static_cast<size_t>(t) * N + j + 8 * q] = bad ? NAN : v[q];
+  }
+  const uint32_t all_l = lane_bits<EPL>(expert_mask_all(N), j);
+  uint32_t taken = ~all_l;
+#pragma unroll 1
+  for (int r = 0; r < k; ++r) {
+    double bv;
+    const int b = grp_best<EPL>(v, ~taken, j, &bv);
+    lane_mark(taken, b, j);
+    if (live && j == 0) {
+      ids[t * k + r] = b;
+      probs[t * k + r] = bv;
+    }
+  }
+}
+
 // ------------------------------------------------------------- launchers
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s, const EpLink* put) {
   EpLink none{};
   return launch_pdl(router_logits_kernel, dim3(T, (N + 7) / 8), dim3(256), 0, s, hidden, wt, d, N, logits,
                     put ? *put : none);
+}
+
+cudaError_t launch_router_route(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, int k,
+                                double* logits, double* full, int32_t* ids, double* probs, cudaStream_t s) {
+  const int cl = (N + 7) / 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl, T);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cl;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, router_route_kernel, hidden, wt, d, N, k, logits, full, ids, probs);
 }
 
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan) {
