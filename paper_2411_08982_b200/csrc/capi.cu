@@ -229,7 +229,7 @@ int check_policy(const lynx_policy_t* pol, int k, int decode, int* floor_keep) {
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? LYNX_OK : LYNX_ERR_CUDA; }
 
 PlanOut plan_out(void* ws, const Plan& P, int n_shared) {
-  PlanOut o;
+  PlanOut o{};
   o.enabled = 1;
   o.n_shared = n_shared;
   o.n_seg = at<int32_t>(ws, P.n_seg);
@@ -280,7 +280,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   int st = cuda_status(launch_gather(ga, sms, s));
   if (st) return st;
 
-  FfnParams fp;
+  FfnParams fp{};
   {
     const uint64_t dw1[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(g.rows1), static_cast<uint64_t>(N + S)};
     const uint64_t dw2[3] = {static_cast<uint64_t>(ff), static_cast<uint64_t>(d), static_cast<uint64_t>(N + S)};
@@ -574,7 +574,7 @@ int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t*
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
   const Caps c = caps_for(T, N, k);
-  PlanOut o;
+  PlanOut o{};
   o.enabled = 1;
   o.n_shared = 0;
   o.n_seg = out->n_seg;
@@ -592,7 +592,7 @@ int lynx_permute(const int32_t* assigned, const double* weights, const uint16_t*
   o.n_counters = 0;
   int st = cuda_status(launch_plan(assigned, weights, T, N, k, o, stream));
   if (st) return st;
-  GatherArgs ga;
+  GatherArgs ga{};
   ga.hidden = hidden;
   ga.perm_token = out->perm_token;
   ga.n_rows = out->n_rows;
@@ -664,7 +664,7 @@ int lynx_attention(const lynx_attention_t* attn, const uint16_t* h_in, int B, in
       attn_out_smem(attn->d_model, attn->d_head, attn->max_len) > 200 * 1024)
     return LYNX_ERR_UNSUPPORTED;
   if (!workspace || workspace_bytes < lynx_attention_workspace_bytes(B * Tn, attn->d_head)) return LYNX_ERR_WORKSPACE;
-  AttnArgs a;
+  AttnArgs a{};
   a.h_in = h_in;
   a.wqkv = attn->wqkv;
   a.wo = attn->wo;

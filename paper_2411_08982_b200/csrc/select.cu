@@ -1022,19 +1022,29 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
         if ((keep >> e) & 1ull) lane_mark(occ, e, j);
       }
 #pragma unroll 1
-      for (int r = 0; r < k; ++r) {  // shuffles stay warp-uniform: every group runs the arg-max
+      for (int r = 0; r < k; ++r) {
         int e = live ? IDS[t * k + r] : 0;
-        double bv;
-        int pick = grp_best<EPL>(v, keep_l & ~occ, j, &bv);
-        if (__any_sync(kFull, pick < 0)) {
-          const int any = grp_best<EPL>(v, keep_l, j, &bv);  // collapse (policy.py:197-200)
-          if (pick < 0) pick = any;
+        const bool disp = !((keep >> e) & 1ull);
+        double val = live ? PROBS[t * k + r] : 0.0;  // p[e] of a kept original (same bits as v)
+        // the arg-max runs only when some group of the warp has slot r
+        // displaced (warp-uniform, so the shuffles stay converged)
+        if (__any_sync(kFull, live && disp)) {
+          double bv;
+          int pick = grp_best<EPL>(v, keep_l & ~occ, j, &bv);
+          if (__any_sync(kFull, pick < 0)) {
+            double bv_any;
+            const int any = grp_best<EPL>(v, keep_l, j, &bv_any);  // collapse (policy.py:197-200)
+            if (pick < 0) {
+              pick = any;
+              bv = bv_any;
+            }
+          }
+          if (disp) {
+            e = pick;
+            lane_mark(occ, e, j);
+            val = bv;
+          }
         }
-        if (!((keep >> e) & 1ull)) {
-          e = pick;
-          lane_mark(occ, e, j);
-        }
-        const double val = grp_at<EPL>(v, e, gbase);
         if (live && j == 0) {
           ASG[t * k + r] = e;
           WT[t * k + r] = val;
