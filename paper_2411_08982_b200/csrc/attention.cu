@@ -82,6 +82,7 @@ __device__ __forceinline__ float row_sumsq(const uint16_t* row, int d, float* re
 
 __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_constant__ AttnArgs a) {
   griddep_launch_dependents();
+  warm_params(a);
   griddep_wait();
   const int row = blockIdx.x;  // b * Tn + i
   const int b = row / a.Tn, i = row - b * a.Tn;
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   __shared__ float qs[LYNX_MAX_DHEAD];
   __shared__ float ctx[LYNX_MAX_DHEAD];
   griddep_launch_dependents();
+  warm_params(a);
   griddep_wait();
   const int row = blockIdx.x;
   const int b = row / a.Tn, i = row - b * a.Tn;

@@ -19,6 +19,7 @@ namespace lynx {
 // planned by K1 (plan_dispatch in select.cu).
 __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ GatherArgs a) {
   griddep_launch_dependents();
+  warm_params(a);
   griddep_wait();
   if (a.ep.enabled) {  // peer-memory EP: every rank's dispatched rows have landed
     if (threadIdx.x == 0) wait_peers(a.ep.P, a.ep.kind, *a.ep.P.epoch + 1);
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ Co
   __shared__ int s_rows[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
   __shared__ float s_w[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
   griddep_launch_dependents();
+  warm_params(a);
   griddep_wait();  // partial slots come from K3
   const int t = blockIdx.y;
   if (threadIdx.x < a.k) {

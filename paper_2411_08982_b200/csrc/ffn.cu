@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
     tma_prefetch_desc(&p.map_x);
     tma_prefetch_desc(&p.map_h);
   }
+  warm_params(p);
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();

@@ -27,6 +27,17 @@ __device__ __forceinline__ void griddep_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Touch every 32-byte line of a __grid_constant__ kernel argument before
+// griddep_wait(): the constant-cache misses of a cold SM then overlap the
+// predecessor's tail instead of stalling the kernel's first uses.
+template <typename A>
+__device__ __forceinline__ void warm_params(const A& a) {
+  constexpr int kLines = static_cast<int>((sizeof(A) + 31) / 32);
+  __shared__ int s_sink;  // a store keeps ptxas from dropping the loads
+  if (static_cast<int>(threadIdx.x) < kLines)
+    *static_cast<volatile int*>(&s_sink) = reinterpret_cast<const int*>(&a)[threadIdx.x * 8];
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {

@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
     s_clipped = 0;
   }
   if (t < N) s_icount[t] = 0;
+  warm_params(a);
   SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
   if (a.ep.enabled) {  // peer-memory EP: every rank's logits rows have landed
@@ -880,6 +881,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
     s_clipped = 0;
   }
   if (tid < N) s_icount[tid] = 0;
+  warm_params(a);
   SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
   if (a.ep.enabled) {  // peer-memory EP: every rank's logits rows have landed
