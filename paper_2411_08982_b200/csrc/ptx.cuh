@@ -25,6 +25,14 @@ __device__ __forceinline__ uint64_t globaltimer() {
 #define LYNX_WATCHDOG_NS 4000000000ull
 #endif
 
+// The report-and-trap path is outlined: every spin loop of the warp-
+// specialised kernels inlines tick(), and their hot loops share the SM's
+// instruction cache.
+static __device__ __noinline__ void watchdog_fire(int code) {
+  printf("lynx watchdog: block %d thread %d stuck at site %d\n", blockIdx.x, threadIdx.x, code);
+  __trap();
+}
+
 struct Watchdog {
   uint64_t start = 0;
   uint32_t iters = 0;
@@ -34,8 +42,7 @@ struct Watchdog {
       if (start == 0) {
         start = now;
       } else if (now - start > LYNX_WATCHDOG_NS) {
-        printf("lynx watchdog: block %d thread %d stuck at site %d\n", blockIdx.x, threadIdx.x, code);
-        __trap();
+        watchdog_fire(code);
       }
     }
   }
