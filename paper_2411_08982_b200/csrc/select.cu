@@ -149,7 +149,7 @@ __device__ __noinline__ void remap_token(const int32_t* ids, const double* p, in
 // [base[e], base[e] + cnt[e]) of the permuted buffer, base 16-aligned;
 // segments split an expert at LYNX_SEG_ROWS rows.  Called by every thread
 // of one CTA; `asg`/`w` may live in shared or global memory.
-__device__ __noinline__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N, int k,
+__device__ __forceinline__ void plan_dispatch(const int32_t* asg, const double* w, int T, int N, int k,
                                            const PlanOut& o, uint32_t* s_bits, int* s_prefix) {
   // The plan's pointers in registers: through the `o` reference every global
   // store below would force a reload of the fields (possible aliasing).
@@ -372,7 +372,7 @@ __host__ __device__ inline SelectSmem select_smem(int T, int N, int k, bool stag
 
 // Batch-level policy: vote, retention order, retained set (policy.py:116-148,
 // 232-338).  Writes s_keep / s_counts; returns via s_clipped.
-__device__ __noinline__ void batch_policy(const SelectArgs& a, const int32_t* IDS, const double* CONF, uint8_t* IMP,
+__device__ __forceinline__ void batch_policy(const SelectArgs& a, const int32_t* IDS, const double* CONF, uint8_t* IMP,
                                           int* s_keep, double* s_counts, int* s_icount, int* s_rank, int* s_order,
                                           int* s_nq, int* s_clipped) {
   const int T = a.T, N = a.N, k = a.k, tid = threadIdx.x, nthr = blockDim.x;
