@@ -851,7 +851,10 @@ __device__ __forceinline__ int grp_best(const double (&v)[EPL], uint32_t cand, i
   return bi == 64 ? -1 : bi;
 }
 
-template <int EPL>
+// kGiven: the selection (ids/probs/full) is an input (a.logits == null; the
+// N > 16 layer path, routed in K0): the softmax / top-k code is compiled
+// out, so the cold kernel's instruction stream runs straight through.
+template <int EPL, bool kGiven>
 __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __grid_constant__ SelectArgs a) {
   __shared__ double s_counts[LYNX_MAX_EXPERTS];
   __shared__ int s_icount[LYNX_MAX_EXPERTS];
@@ -897,7 +900,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   for (int t = grp; t < Tw; t += ngrp) {
     const bool live = t < T;
     double v[EPL];
-    if (a.logits) {
+    if (!kGiven) {
       const double* z = a.logits + static_cast<size_t>(t) * N;
       bool bad = false;
       double m = -INFINITY;
@@ -1387,19 +1390,28 @@ cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
   }
   // Group path: every other shape (N <= 64, or rows too large to stage),
   // eight lanes per token.
-  static int configured32 = -1, configured64 = -1;
+  const bool given = a.logits == nullptr;
+  const void* fn;
+  static int configured[4] = {-1, -1, -1, -1};
+  int* conf;
   if (a.N <= 32) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<4>), configured32);
-      if (e != cudaSuccess) return e;
-    }
-    return launch_pdl(route_select_group<4>, dim3(1), dim3(kSelectThreads), smem, s, a);
+    fn = given ? reinterpret_cast<const void*>(route_select_group<4, true>)
+               : reinterpret_cast<const void*>(route_select_group<4, false>);
+    conf = &configured[given ? 1 : 0];
+  } else {
+    fn = given ? reinterpret_cast<const void*>(route_select_group<8, true>)
+               : reinterpret_cast<const void*>(route_select_group<8, false>);
+    conf = &configured[given ? 3 : 2];
   }
   if (smem > 48 * 1024) {
-    cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_group<8>), configured64);
+    cudaError_t e = allow_big_smem(fn, *conf);
     if (e != cudaSuccess) return e;
   }
-  return launch_pdl(route_select_group<8>, dim3(1), dim3(kSelectThreads), smem, s, a);
+  if (a.N <= 32)
+    return given ? launch_pdl(route_select_group<4, true>, dim3(1), dim3(kSelectThreads), smem, s, a)
+                 : launch_pdl(route_select_group<4, false>, dim3(1), dim3(kSelectThreads), smem, s, a);
+  return given ? launch_pdl(route_select_group<8, true>, dim3(1), dim3(kSelectThreads), smem, s, a)
+               : launch_pdl(route_select_group<8, false>, dim3(1), dim3(kSelectThreads), smem, s, a);
 }
 
 cudaError_t launch_plan(const int32_t* asg, const double* w, int T, int N, int k, const PlanOut& o, cudaStream_t s) {
