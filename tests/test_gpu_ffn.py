@@ -371,3 +371,35 @@ def test_random_layer_configs_vs_oracle(seed):
     ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights,
                            round_h_bf16=True, shared=range(N, N + S))
     assert O.norm_rel_err(_np(y), ref) <= TOL, tag
+
+
+@pytest.mark.parametrize("T,N,k,S,mode", [(4096, 64, 8, 2, "accuracy"), (4096, 64, 8, 0, "latency"),
+                                          (4096, 8, 2, 0, "latency"), (1024, 33, 5, 1, "accuracy")])
+def test_layer_at_maximum_sizes_vs_oracle(T, N, k, S, mode):
+    """The whole layer at the ABI limits (T <= 4096, N <= 64, k <= 8): K1
+    works in global memory when its per-token arrays do not fit in shared
+    memory, segments split at LYNX_SEG_ROWS, and the K3 queue holds more
+    segments than K1 ranks in shared memory."""
+    d, ff = 128, 64
+    cfg = (L.PolicyConfig(mode="latency", drop_count=N // 2) if mode == "latency"
+           else L.PolicyConfig(mode="accuracy", freq_keep_budget=N // 3))
+    opol = (O.Policy(mode="latency", drop_count=N // 2) if mode == "latency"
+            else O.Policy(mode="accuracy", freq_keep_budget=N // 3))
+    spec = L.MoEModelSpec(1, N, k, d, ff, num_shared_experts=S)
+    model = L.build_swiglu_model(spec, seed=7)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    hidden = torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16)
+    layer = L.LynxMoELayer(model, 0, T, policy=cfg)
+    y = layer(hidden)
+    torch.cuda.synchronize()
+    logits = _np(L.router_logits(model, 0, hidden))
+    ids, probs, full = O.route(logits, k)
+    ref_mask = O.apply(ids, probs, full, opol)
+    assert np.array_equal(_np(layer.expert_ids), ids)
+    assert np.array_equal(_np(layer.assigned), ref_mask.assigned)
+    assert np.allclose(_np(layer.weights), ref_mask.weights, rtol=1e-12, atol=1e-15)
+    w1, w3 = L.unpack_w13(model.w13[0], ff)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights,
+                           round_h_bf16=True, shared=range(N, N + S))
+    assert O.norm_rel_err(_np(y), ref) <= TOL
