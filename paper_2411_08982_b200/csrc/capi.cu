@@ -132,7 +132,7 @@ Geometry geometry(const lynx_layer_t* L, int T) {
 // Workspace carve-up.  Selection region only for the whole-layer call.
 struct Plan {
   size_t logits, ids, probs, full, conf, counts, retained, assigned, weights, important, flags;
-  size_t n_seg, n_used, n_rows, seg_expert, seg_row, seg_count, seg_order, perm_token, perm_weight, tok_rows,
+  size_t n_seg, n_used, n_rows, max_rows, seg_expert, seg_row, seg_count, seg_order, perm_token, perm_weight, tok_rows,
       tok_weight;
   size_t counters, x_perm, h, y;
   size_t total;
@@ -166,6 +166,7 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
   p.n_seg = take(sizeof(int32_t));
   p.n_used = take(sizeof(int32_t));
   p.n_rows = take(sizeof(int32_t));
+  p.max_rows = take(sizeof(int32_t));
   p.seg_expert = take(sizeof(int32_t) * c.max_seg);
   p.seg_row = take(sizeof(int32_t) * c.max_seg);
   p.seg_count = take(sizeof(int32_t) * c.max_seg);
@@ -235,6 +236,7 @@ PlanOut plan_out(void* ws, const Plan& P, int n_shared) {
   o.n_seg = at<int32_t>(ws, P.n_seg);
   o.n_used = at<int32_t>(ws, P.n_used);
   o.n_rows = at<int32_t>(ws, P.n_rows);
+  o.max_rows = at<int32_t>(ws, P.max_rows);
   o.seg_expert = at<int32_t>(ws, P.seg_expert);
   o.seg_row = at<int32_t>(ws, P.seg_row);
   o.seg_count = at<int32_t>(ws, P.seg_count);
@@ -298,6 +300,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.seg_row = o.seg_row;
   fp.seg_count = o.seg_count;
   fp.seg_order = o.seg_order;
+  fp.max_rows = o.max_rows;
   fp.h = at<uint16_t>(ws, P.h);
   fp.partial = at<float>(ws, P.y);
   fp.counters = o.counters;

@@ -49,6 +49,11 @@ constexpr int kFfnThreads = 256;
 constexpr int kUnitRing = 4;
 constexpr int kTileA = 128 * 64 * 2;  // 128 weight rows x 64 bf16 (one 128B-swizzled k block)
 constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
+// Stage geometry is set at run time from the plan's widest segment: the
+// launch's template BN (from T) sizes shared memory and TMEM, but a stage
+// only needs 16 KB of weights + 2 KB per 16 rows of the widest segment, so a
+// batch whose experts got few rows each runs more stages in the same bytes.
+constexpr int kMaxStages = 12;
 
 struct Unit {
   int phase, seg, mt, split, kb0, kb1, expert, row0, n, nmma;
@@ -116,13 +121,12 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_constant__ FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kTileB = BN * 128;
+  constexpr int kRing = STAGES * (kTileA + BN * 128);
   constexpr uint32_t kTmemCols = 2 * BN;
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * kTileA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kTileB);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* ring = smem;  // stage s: [weights 16 KB | token rows], s * stage_bytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRing);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* ufull = tempty + 2;
   uint64_t* uempty = ufull + kUnitRing;
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   // critical path (K4 still reads nothing before this grid completes).
   griddep_launch_dependents();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -168,6 +172,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 #endif
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
+  const int width = p.max_rows ? min(BN, max(16, (*p.max_rows + 15) & ~15)) : BN;
+  const int stage_bytes = kTileA + width * 128;
+  const int nstages = min(kMaxStages, kRing / stage_bytes);
   const int total = nseg * (p.tiles1 + p.tiles2 * p.split2);
 
   if (warp == 0) {
@@ -207,10 +214,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
           mbar_expect_tx(&full[stage], bytes);
-          tma_load_3d(sA + stage * kTileA, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
+          uint8_t* sa = ring + stage * stage_bytes;
+          tma_load_3d(sa, ma, &full[stage], kb * 64, U.mt * 128, U.expert, pol_w);
           for (int j = 0; j < nb; ++j)
-            tma_load_2d(sB + stage * kTileB + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
-          if (++stage == STAGES) {
+            tma_load_2d(sa + kTileA + j * kBoxB, mb, &full[stage], kb * 64, U.row0 + 16 * j, pol_act);
+          if (++stage == nstages) {
             stage = 0;
             phase ^= 1;
           }
@@ -240,13 +248,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&full[stage], phase, 6);
           tc_fence_after();
-          const uint64_t ad = sdesc_kmajor_sw128(smem_u32(sA + stage * kTileA));
-          const uint64_t bd = sdesc_kmajor_sw128(smem_u32(sB + stage * kTileB));
+          const uint32_t sa = smem_u32(ring + stage * stage_bytes);
+          const uint64_t ad = sdesc_kmajor_sw128(sa);
+          const uint64_t bd = sdesc_kmajor_sw128(sa + kTileA);
 #pragma unroll
           for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide block; +32 B = +2 in the address field
             umma_bf16_ss(dt, ad + 2 * k, bd + 2 * k, idesc, (kb > U.kb0 || k > 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
-          if (++stage == STAGES) {
+          if (++stage == nstages) {
             stage = 0;
             phase ^= 1;
           }
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
 template <int BN, int STAGES>
 static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s) {
   constexpr size_t smem =
-      1024 + STAGES * (kTileA + BN * 128) + (2 * STAGES + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
+      1024 + STAGES * (kTileA + BN * 128) + (2 * kMaxStages + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static int configured_device = -1;
   int dev = 0;

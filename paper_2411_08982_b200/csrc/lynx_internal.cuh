@@ -70,6 +70,7 @@ struct PlanOut {
   int32_t* n_seg;
   int32_t* n_used;
   int32_t* n_rows;      // rows of the permuted buffer in use (16-padded per expert)
+  int32_t* max_rows;    // rows of the largest segment (K3's stage width), or null
   int32_t* seg_expert;
   int32_t* seg_row;
   int32_t* seg_count;
@@ -114,6 +115,7 @@ struct FfnParams {
   const int32_t* seg_row;
   const int32_t* seg_count;
   const int32_t* seg_order;  // queue slot -> segment (largest first)
+  const int32_t* max_rows;   // rows of the largest segment, or null (-> the launch's BN)
   uint16_t* h;      // [rows_cap, ff] bf16
   float* partial;   // [split2, rows_cap, d] f32
   int* counters;    // [0] unit ticket, [1 + s] phase-0 tiles done for segment s

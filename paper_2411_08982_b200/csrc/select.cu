@@ -156,6 +156,7 @@ __device__ __forceinline__ void plan_dispatch(const int32_t* asg, const double* 
   int32_t* __restrict__ const o_n_seg = o.n_seg;
   int32_t* __restrict__ const o_n_used = o.n_used;
   int32_t* __restrict__ const o_n_rows = o.n_rows;
+  int32_t* __restrict__ const o_max_rows = o.max_rows;
   int32_t* __restrict__ const o_seg_expert = o.seg_expert;
   int32_t* __restrict__ const o_seg_row = o.seg_row;
   int32_t* __restrict__ const o_seg_count = o.seg_count;
@@ -252,8 +253,13 @@ __device__ __forceinline__ void plan_dispatch(const int32_t* asg, const double* 
       o_seg_count[seg_off + i] = rows;
       if (seg_off + i < kOrderMax) s_segcnt[seg_off + i] = rows;
     }
+    // widest segment (K3 sizes its pipeline stages by it)
+    int widest = max(min(cnt[0], LYNX_SEG_ROWS), min(cnt[1], LYNX_SEG_ROWS));
+    widest = __reduce_max_sync(kFull, widest);
+    if (S > 0) widest = max(widest, min(T, LYNX_SEG_ROWS));
     if (lane == 0) {
       s_shared_base = row_off;
+      if (o_max_rows) *o_max_rows = widest;
       *o_n_seg = seg_off + S * seg_per_shared;
       *o_n_used = nused + S;
       *o_n_rows = row_off + S * T16;
