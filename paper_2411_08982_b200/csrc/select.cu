@@ -809,10 +809,9 @@ __device__ __forceinline__ double grp_pairwise(const double (&v)[EPL], int n, in
 // Lane-local candidate masks: bit m of lane j's mask <-> expert j + 8m.
 template <int EPL>
 __device__ __forceinline__ uint32_t lane_bits(uint64_t mask, int j) {
-  uint32_t l = 0;
-#pragma unroll
-  for (int m = 0; m < EPL; ++m) l |= static_cast<uint32_t>((mask >> (j + 8 * m)) & 1ull) << m;
-  return l;
+  // the low bit of every byte of mask >> j, packed by one multiply
+  const uint64_t x = (mask >> j) & 0x0101010101010101ull;
+  return static_cast<uint32_t>((x * 0x0102040810204080ull) >> 56) & ((1u << EPL) - 1u);
 }
 
 __device__ __forceinline__ void lane_mark(uint32_t& l, int e, int j) {
@@ -1072,16 +1071,17 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
     }
     __syncwarp();
     SEL_TS_LOCAL(23);
+    // row sum on lane 0 (numpy's pairwise order), then lane r divides slot r
+    double total = 0.0;
     if (live && j == 0) {
       double slot[LYNX_MAX_TOPK];
 #pragma unroll
       for (int r = 0; r < LYNX_MAX_TOPK; ++r) slot[r] = r < k ? WT[t * k + r] : 0.0;
-      const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot, k);
+      total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot, k);
       if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);
-#pragma unroll
-      for (int r = 0; r < LYNX_MAX_TOPK; ++r)
-        if (r < k) WT[t * k + r] = slot[r] / total;
     }
+    total = __shfl_sync(kFull, total, gbase);
+    if (live && j < k) WT[t * k + j] = WT[t * k + j] / total;
   }
   __syncthreads();
   SEL_TS(4);
