@@ -856,6 +856,61 @@ __device__ __forceinline__ int grp_best(const double (&v)[EPL], uint32_t cand, i
   return bi == 64 ? -1 : bi;
 }
 
+// remap_tokens for one token row (policy.py:171-210) on the group layout,
+// over the COMPACT retained list: candidate c (lane c % 8, slot c / 8) is
+// the c-th retained expert ascending, so (p desc, c asc) is the reference's
+// (p desc, expert asc) and the arg-max scans EPR = ceil(|R| / 8) values per
+// lane instead of one per expert.  Displaced slots take the best retained,
+// unoccupied expert, else collapse onto the best retained one.  Writes the
+// assignment and the slot probability (renormalised by the caller).
+template <int EPR>
+__device__ __forceinline__ void remap_row(const double* prow, bool live, int t, int k, int j, uint64_t keep, int nR,
+                                          const int* rlist, const int32_t* IDS, const double* PROBS, int32_t* ASG,
+                                          double* WT) {
+  double v[EPR];
+#pragma unroll
+  for (int q = 0; q < EPR; ++q) {
+    const int c = j + 8 * q;
+    v[q] = (live && c < nR) ? prow[rlist[c]] : 0.0;
+  }
+  const uint32_t all_c = lane_bits<EPR>(nR >= 64 ? ~0ull : ((1ull << nR) - 1ull), j);
+  uint32_t occ = 0;  // lane-local: retained original choices (compact indices)
+#pragma unroll 1
+  for (int r = 0; r < k; ++r) {
+    const int e = live ? IDS[t * k + r] : 0;
+    if ((keep >> e) & 1ull) lane_mark(occ, __popcll(keep & ((1ull << e) - 1ull)), j);
+  }
+#pragma unroll 1
+  for (int r = 0; r < k; ++r) {
+    int e = live ? IDS[t * k + r] : 0;
+    const bool disp = !((keep >> e) & 1ull);
+    double val = live ? PROBS[t * k + r] : 0.0;  // p[e] of a kept original (same bits as v)
+    // the arg-max runs only when some group of the warp has slot r displaced
+    // (warp-uniform, so the shuffles stay converged)
+    if (__any_sync(kFull, live && disp)) {
+      double bv;
+      int pick = grp_best<EPR>(v, all_c & ~occ, j, &bv);
+      if (__any_sync(kFull, pick < 0)) {
+        double bv_any;
+        const int any = grp_best<EPR>(v, all_c, j, &bv_any);  // collapse (policy.py:197-200)
+        if (pick < 0) {
+          pick = any;
+          bv = bv_any;
+        }
+      }
+      if (disp) {
+        if (pick >= 0) lane_mark(occ, pick, j);
+        e = pick >= 0 ? rlist[pick] : -1;
+        val = bv;
+      }
+    }
+    if (live && j == 0) {
+      ASG[t * k + r] = e;
+      WT[t * k + r] = val;
+    }
+  }
+}
+
 // kGiven: the selection (ids/probs/full) is an input (a.logits == null; the
 // N > 16 layer path, routed in K0): the softmax / top-k code is compiled
 // out, so the cold kernel's instruction stream runs straight through.
@@ -868,6 +923,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   __shared__ int s_keep[LYNX_MAX_EXPERTS];
   __shared__ int s_flags, s_nq, s_clipped;
   __shared__ unsigned long long s_keepmask;
+  __shared__ int s_rlist[LYNX_MAX_EXPERTS];  // retained experts ascending
   extern __shared__ __align__(16) uint8_t s_dyn[];
 
   griddep_launch_dependents();
@@ -1002,7 +1058,13 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   if (tid < 32) {  // retained bitmask: one ballot per 32 experts
     const unsigned lo = __ballot_sync(kFull, tid < N && s_keep[tid]);
     const unsigned hi = __ballot_sync(kFull, tid + 32 < N && s_keep[tid + 32]);
-    if (tid == 0) s_keepmask = (static_cast<unsigned long long>(hi) << 32) | lo;
+    const unsigned long long km = (static_cast<unsigned long long>(hi) << 32) | lo;
+    if (tid == 0) s_keepmask = km;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = tid + 32 * h;
+      if ((km >> e) & 1ull) s_rlist[__popcll(km & ((1ull << e) - 1ull))] = e;
+    }
   }
   __syncthreads();
   SEL_TS(3);
@@ -1010,7 +1072,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   // 2) remap onto the retained set (policy.py:171-210), or the identity
   // mask with weights = probs / row sum (policy.py:215-229)
   const uint64_t keep = s_keepmask;
-  const uint32_t keep_l = lane_bits<EPL>(keep, j);
+  const int nR = __popcll(keep);
   SEL_TS_LOCAL(20);
 #pragma unroll 1
   for (int t = grp; t < Tw; t += ngrp) {
@@ -1019,48 +1081,11 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
       // rolled slot loop (one inlined arg-max): the kernel runs from a cold
       // instruction cache once per layer, so code size is latency.  Slot
       // probabilities park in WT until the row's renormalisation.
-      double v[EPL];
-#pragma unroll
-      for (int q = 0; q < EPL; ++q) {
-        const int e = j + 8 * q;
-        v[q] = (live && e < N) ? P[static_cast<size_t>(t) * N + e] : 0.0;
-      }
-      uint32_t occ = 0;  // lane-local: retained original choices
-#pragma unroll 1
-      for (int r = 0; r < k; ++r) {
-        const int e = live ? IDS[t * k + r] : 0;
-        if ((keep >> e) & 1ull) lane_mark(occ, e, j);
-      }
-#pragma unroll 1
-      for (int r = 0; r < k; ++r) {
-        int e = live ? IDS[t * k + r] : 0;
-        const bool disp = !((keep >> e) & 1ull);
-        double val = live ? PROBS[t * k + r] : 0.0;  // p[e] of a kept original (same bits as v)
-        // the arg-max runs only when some group of the warp has slot r
-        // displaced (warp-uniform, so the shuffles stay converged)
-        if (__any_sync(kFull, live && disp)) {
-          double bv;
-          int pick = grp_best<EPL>(v, keep_l & ~occ, j, &bv);
-          if (__any_sync(kFull, pick < 0)) {
-            double bv_any;
-            const int any = grp_best<EPL>(v, keep_l, j, &bv_any);  // collapse (policy.py:197-200)
-            if (pick < 0) {
-              pick = any;
-              bv = bv_any;
-            }
-          }
-          if (disp) {
-            e = pick;
-            lane_mark(occ, e, j);
-            val = bv;
-          }
-        }
-        if (live && j == 0) {
-          ASG[t * k + r] = e;
-          WT[t * k + r] = val;
-        }
-        if (r == 0) SEL_TS_LOCAL(21);
-      }
+      const double* prow = P + static_cast<size_t>(t) * N;
+      if (EPL > 4 && nR <= 32)
+        remap_row<(EPL > 4 ? 4 : EPL)>(prow, live, t, k, j, keep, nR, s_rlist, IDS, PROBS, ASG, WT);
+      else
+        remap_row<EPL>(prow, live, t, k, j, keep, nR, s_rlist, IDS, PROBS, ASG, WT);
       SEL_TS_LOCAL(22);
     } else if (live && j == 0) {
 #pragma unroll 1
