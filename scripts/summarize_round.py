@@ -1,0 +1,117 @@
+"""Summarise a round's GPU evidence from gpurun_out/ into profiles/ (runs
+here, no GPU): bench lines, the ncu launch list, the ncu --set full metrics of
+each captured kernel, K3's DRAM traffic and the SASS mnemonics.
+    python scripts/summarize_round.py r01"""
+import collections
+import csv
+import io
+import json
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
+           "launch__shared_mem_per_block", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def short(name):
+    name = re.sub(r"\(.*$", "", name.replace("void ", ""))
+    return re.sub(r"\(int\)|\(bool\)", "", name)
+
+
+def launches(tag):
+    rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
+    hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hdr]
+    ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    per = collections.defaultdict(list)
+    for r in rows[hdr + 1:]:
+        if len(r) > vi and r[mi] == "gpu__time_duration.sum" and "lynx::" in r[ki]:
+            per[short(r[ki])].append(float(r[vi].replace(",", "")) / 1e3)  # ns -> us
+    tot = sum(sum(v) for v in per.values())
+    lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none), round {tag[1:]}",
+             "# command: ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv python bench.py "
+             "--steps 20 --warmup 3 --no-cpu-baseline",
+             "# cold-cache, serialised replays: compare SHARES of the step, not absolutes",
+             f"{'kernel':40s} {'launches':>9s} {'mean_us':>9s} {'min_us':>9s} {'share':>7s}"]
+    for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"{k:40s} {len(v):9d} {sum(v) / len(v):9.2f} {min(v):9.2f} {100 * sum(v) / tot:6.1f}%")
+    open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def ncu_raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = {"Kernel Name": r[h.index("Kernel Name")]}
+        for m in METRICS:
+            if m in h:
+                i = h.index(m)
+                d[m] = f"{r[i]} {units[i]}".strip()
+        out.append(d)
+    return out
+
+
+def to_bytes(s):
+    v, u = s.split()
+    return float(v.replace(",", "")) * UNIT[u]
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    for f in sorted(os.listdir(OUT)):
+        if f.startswith("bench_") and f.endswith(".json") and os.path.getsize(os.path.join(OUT, f)):
+            shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
+    for f in ("timeline_c2.json", "timeline_c4.json"):
+        if os.path.exists(os.path.join(OUT, f)) and os.path.getsize(os.path.join(OUT, f)):
+            shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
+    if os.path.exists(os.path.join(OUT, "timeline_stack.json")):
+        shutil.copy(os.path.join(OUT, "timeline_stack.json"), os.path.join(PROF, f"{tag}_timeline_stack_c3.json"))
+    launches(tag)
+    kernels = []
+    for rep in ("ffn_full.ncu-rep", "small_full.ncu-rep"):
+        if os.path.exists(os.path.join(OUT, rep)):
+            kernels += ncu_raw(os.path.join(OUT, rep))
+    shutil.copy(os.path.join(OUT, "ffn_full.ncu-rep"), os.path.join(PROF, f"{tag}_ffn_full.ncu-rep"))
+    summary = {
+        "what": "ncu --set full --clock-control none captures of one C2 layer step (Mixtral-8x7B shape, T=32, "
+                "Lynx latency drop 4, 4 used experts)",
+        "commands": ["scripts/ncu_round.sh"],
+        "note": "per-kernel times are cold-cache replays; ffn_kernel DRAM read vs 1.409 GB algorithmic "
+                "(4 x 3*d*ff*2): only the used experts are streamed, each once",
+        "kernels": kernels}
+    json.dump(summary, open(os.path.join(PROF, f"{tag}_ncu_full_summary.json"), "w"), indent=1)
+    ffn = next(k for k in kernels if "ffn_kernel" in k["Kernel Name"])
+    rd, wr = to_bytes(ffn["dram__bytes_read.sum"]), to_bytes(ffn["dram__bytes_write.sum"])
+    json.dump({"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+               "source": f"ncu --set full, profiles/{tag}_ncu_full_summary.json (ffn_kernel, C2 Lynx drop 4, "
+                         "4 used experts)", "algorithmic_bytes_per_launch": 4 * 3 * 4096 * 14336 * 2},
+              open(os.path.join(PROF, "ffn_traffic.json"), "w"), indent=1)
+    print(json.dumps({k["Kernel Name"][:40]: k["gpu__time_duration.sum"] for k in kernels}, indent=1))
+    sass = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "build", "ffn.o")], capture_output=True,
+                          text=True).stdout
+    ops = collections.Counter(m.group(1) for m in re.finditer(r"/\*[0-9a-f]{4,}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Za-z0-9_.]+)",
+                                                               sass))
+    keep = {o: c for o, c in ops.items() if re.match(r"UTC|UTMA|LDTM|SYNCS|HMMA", o)}
+    lines = [f"# SASS evidence (cuobjdump -sass build/ffn.o, all ffn_kernel<BN,STAGES> instances), round {tag[1:]}",
+             "# tcgen05.mma -> UTCHMMA, tcgen05.ld -> LDTM, TMA -> UTMALDG, mbarriers -> SYNCS; "
+             "no HMMA (legacy mma.sync) anywhere"]
+    lines += [f"{c:7d} {o}" for o, c in sorted(keep.items(), key=lambda kv: -kv[1])]
+    open(os.path.join(PROF, f"{tag}_sass_evidence.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
