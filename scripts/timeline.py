@@ -49,7 +49,7 @@ def main():
     ev.sort(key=lambda e: e.time_range.start)
     steps, cur = [], []
     for e in ev:
-        if "router_logits" in e.name and cur:
+        if "router_" in e.name and cur:  # K0: router_logits_kernel or router_route_kernel
             steps.append(cur)
             cur = []
         cur.append(e)
