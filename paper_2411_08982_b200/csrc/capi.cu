@@ -256,9 +256,11 @@ inline void record(cudaEvent_t const* ev, int i, cudaStream_t s) {
 
 // K2 gather -> K3 expert GEMM + combine, on a plan already in the workspace.
 // ev (optional): [0] before K2 (gather), [1] before K3 (FFN), [2] before K4 (combine).
+// kept_hint: experts expected to stay in use (the policy's kept-set size;
+// N when unknown), for K3's kernel choice only.
 int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_t* out_bf16, float* out_f32,
                    void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev,
-                   const lynx_ep_peers_t* peers = nullptr) {
+                   const lynx_ep_peers_t* peers = nullptr, int kept_hint = 0) {
   const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff, S = L->num_shared;
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
@@ -315,7 +317,8 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   fp.kb2_total = g.kb2_total;
   fp.rows_cap = c.rows_cap;
   record(ev, 1, s);
-  st = cuda_status(launch_ffn(fp, g.bn, sms, s));
+  const int kept = kept_hint > 0 ? std::min(kept_hint, N) : N;
+  st = cuda_status(launch_ffn(fp, g.bn, T * k / kept, sms, s));
   if (st) return st;
 
   CombineArgs ca{};
@@ -435,7 +438,13 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   record(ev, 1, stream);
   st = cuda_status(launch_route_select(a, stream));
   if (st) return st;
-  st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr);
+  // experts the policy is expected to keep (K3's kernel choice; no effect on results)
+  int kept = N;
+  if (policy && decode && policy->mode == LYNX_POLICY_LATENCY)
+    kept = std::max(floor_keep, N - policy->drop_count);
+  else if (policy && decode && policy->mode == LYNX_POLICY_ACCURACY)
+    kept = std::max(floor_keep, policy->freq_keep_budget);
+  st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr, nullptr, kept);
   record(ev, 5, stream);
   return st;
 }

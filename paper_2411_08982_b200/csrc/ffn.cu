@@ -39,6 +39,7 @@
 //   warps 4..7  epilogue: TMEM -> registers -> activation -> global
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lynx_internal.cuh"
 #include "ptx.cuh"
@@ -361,6 +362,358 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   }
 }
 
+// ------------------------------------------- CTA-pair variant (large T)
+// The same unit queue, run by clusters of two CTAs on one TPC with
+// tcgen05.mma.cta_group::2: a unit is 256 weight rows (CTA r stages rows
+// 128r..128r+127 of it) against the segment's tokens, of which each CTA
+// stages half.  The leader (rank 0) issues the M=256 MMA; every CTA's TMEM
+// holds its 128 weight rows x all tokens, so the epilogue is per CTA as in
+// the single-CTA kernel.  Per weight byte each SM stages half the token rows
+// of the single-CTA kernel: at large batches the activation tiles are as
+// large as the weight tiles and their L2 traffic caps the stream.
+//
+// Handshakes: the leader's producer takes the tickets and writes them into
+// both CTAs' unit rings; both producers wait for their own ring stage to be
+// empty (the MMA commit is multicast to both CTAs) and complete their bytes
+// on the leader's full barrier; both CTAs' epilogues arrive on the leader's
+// accumulator-empty and unit-empty barriers.
+__device__ __forceinline__ bool decode_unit_pair(const FfnParams& p, int nseg, int u, int tp1, int tp2, Unit& U) {
+  if (u < 0) return false;
+  const int nA = nseg * tp1;
+  int slot;
+  if (u < nA) {
+    U.phase = 0;
+    slot = u / tp1;
+    U.mt = u - slot * tp1;  // pair tile: CTA r takes 128-row tile 2 * mt + r
+    U.split = 0;
+    U.kb0 = 0;
+    U.kb1 = p.kb1;
+  } else {
+    const int v = u - nA;
+    const int per = tp2 * p.split2;
+    U.phase = 1;
+    slot = v / per;
+    const int r = v - slot * per;
+    U.mt = r / p.split2;
+    U.split = r - U.mt * p.split2;
+    U.kb0 = U.split * p.kb2_per;
+    U.kb1 = min(p.kb2_total, U.kb0 + p.kb2_per);
+  }
+  U.seg = p.seg_order[slot];
+  U.expert = p.seg_expert[U.seg];
+  U.row0 = p.seg_row[U.seg];
+  U.n = p.seg_count[U.seg];
+  U.nmma = (U.n + 31) & ~31;  // even split of the token rows over the pair
+  return true;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_constant__ FfnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kRing = STAGES * (kTileA + BN * 64);
+  constexpr uint32_t kTmemCols = 2 * BN;
+  uint8_t* ring = smem;  // stage s: [weights 16 KB | this CTA's half of the token rows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRing);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tfull = empty + kMaxStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ufull = tempty + 2;
+  uint64_t* uempty = ufull + kUnitRing;
+  int* uring = reinterpret_cast<int*>(uempty + kUnitRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // multicast MMA commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // leader: 4 epilogue warps x 2 CTAs
+    }
+    for (int i = 0; i < kUnitRing; ++i) {
+      mbar_init(&ufull[i], 1);
+      mbar_init(&uempty[i], 10);  // leader: MMA + 4 epilogue warps, peer: producer + 4 epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (threadIdx.x == 32) {
+    tma_prefetch_desc(&p.map_w1);
+    tma_prefetch_desc(&p.map_w2);
+    tma_prefetch_desc(&p.map_x);
+    tma_prefetch_desc(&p.map_h);
+  }
+  warm_params(p);
+  if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  griddep_wait();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nseg = *p.n_seg;
+  const int tp1 = (p.tiles1 + 1) >> 1, tp2 = (p.tiles2 + 1) >> 1;
+  const int total = nseg * (tp1 + tp2 * p.split2);
+  const int width = p.max_rows ? min(BN, max(32, (*p.max_rows + 31) & ~31)) : BN;
+  const int stage_bytes = kTileA + (width >> 1) * 128;
+  const int nstages = min(kMaxStages, kRing / stage_bytes);
+  const uint32_t peer_ufull = mapa_shared(ufull, 1), peer_uring = mapa_shared(uring, 1);
+  const uint32_t lead_uempty = mapa_shared(uempty, 0), lead_tempty = mapa_shared(tempty, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producers (both CTAs)
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_act = policy_evict_last();
+      int stage = 0, slot = 0;
+      uint32_t phase = 0, uphase = 0;
+      while (true) {
+        int u;
+        if (leader) {
+          u = atomicAdd(&p.counters[0], 1);
+          if (u >= total) u = -1;
+          mbar_wait(&uempty[slot], uphase ^ 1, 1);
+          uring[slot] = u;
+          st_cluster_u32(peer_uring + 4 * slot, static_cast<uint32_t>(u));
+          mbar_arrive(&ufull[slot]);
+          mbar_arrive_cluster(peer_ufull + 8 * slot);
+        } else {
+          mbar_wait_cluster(&ufull[slot], uphase, 1);
+          u = uring[slot];
+          mbar_arrive_cluster(lead_uempty + 8 * slot);
+        }
+        if (++slot == kUnitRing) {
+          slot = 0;
+          uphase ^= 1;
+        }
+        Unit U;
+        if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
+        const CUtensorMap* ma = U.phase == 0 ? &p.map_w1 : &p.map_w2;
+        const CUtensorMap* mb = U.phase == 0 ? &p.map_x : &p.map_h;
+        if (U.phase == 1) {
+          const int* done = p.counters + 1 + U.seg;
+          Watchdog wd;
+          while (ld_acquire_gpu(done) < 4 * p.tiles1) {
+            __nanosleep(100);
+            wd.tick(2);
+          }
+          fence_proxy_async();  // H was written by generic stores; TMA reads it
+        }
+        const int half = U.nmma >> 1;  // token rows per CTA
+        const int nb = half >> 4;
+        const uint32_t bytes = 2 * (kTileA + nb * kBoxB);  // both CTAs' bytes land on the leader's barrier
+        const int wrow = (2 * U.mt + static_cast<int>(rank)) * 128;
+        const int trow = U.row0 + static_cast<int>(rank) * half;
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1, 3);
+          if (leader) mbar_expect_tx(&full[stage], bytes);
+          uint8_t* sa = ring + stage * stage_bytes;
+          tma_load_3d_pair(sa, ma, &full[stage], kb * 64, wrow, U.expert, pol_w);
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d_pair(sa + kTileA + j * kBoxB, mb, &full[stage], kb * 64, trow + 16 * j, pol_act);
+          if (++stage == nstages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      int stage = 0, slot = 0, acc = 0;
+      uint32_t phase = 0, uphase = 0, aphase = 0;
+      while (true) {
+        mbar_wait(&ufull[slot], uphase, 4);
+        const int u = uring[slot];
+        mbar_arrive(&uempty[slot]);
+        if (++slot == kUnitRing) {
+          slot = 0;
+          uphase ^= 1;
+        }
+        Unit U;
+        if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
+        const uint32_t idesc = idesc_bf16_f32(256, U.nmma);
+        mbar_wait_cluster(&tempty[acc], aphase ^ 1, 5);
+        tc_fence_after();
+        const uint32_t dt = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+          mbar_wait(&full[stage], phase, 6);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(ring + stage * stage_bytes);
+          const uint64_t ad = sdesc_kmajor_sw128(sa);
+          const uint64_t bd = sdesc_kmajor_sw128(sa + kTileA);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide block; +32 B = +2 in the address field
+            umma_bf16_ss_pair(dt, ad + 2 * k, bd + 2 * k, idesc, (kb > U.kb0 || k > 0) ? 1u : 0u);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == nstages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------- epilogue (both CTAs)
+    const int q = warp - 4;  // TMEM lane quarter (warp_id % 4)
+    int slot = 0, acc = 0;
+    uint32_t uphase = 0, aphase = 0;
+    while (true) {
+      if (leader) mbar_wait(&ufull[slot], uphase, 7);
+      else mbar_wait_cluster(&ufull[slot], uphase, 7);
+      const int u = uring[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&uempty[slot]);
+        else mbar_arrive_cluster(lead_uempty + 8 * slot);
+      }
+      if (++slot == kUnitRing) {
+        slot = 0;
+        uphase ^= 1;
+      }
+      Unit U;
+      if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
+      mbar_wait(&tfull[acc], aphase, 8);
+      tc_fence_after();
+      const int tile = 2 * U.mt + static_cast<int>(rank);
+      const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      if (U.phase == 0) {
+        const bool real = tile < p.tiles1;  // the second tile of an odd count is padding
+        __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(p.h);
+        if (p.act == LYNX_ACT_SWIGLU) {
+          const int f = tile * 64 + q * 16 + (lane & 15);
+          const bool upper = lane >= 16;
+          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tb + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float send = __uint_as_float(upper ? v[j] : v[8 + j]);
+              const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+              const float g = upper ? recv : __uint_as_float(v[j]);
+              const float uu = upper ? __uint_as_float(v[8 + j]) : recv;
+              const int tok = c0 + (upper ? 8 : 0) + j;
+              if (real && tok < U.n && f < p.ff)
+                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(silu_mul(g, uu));
+            }
+          }
+        } else {
+          const int f = tile * 128 + q * 32 + lane;
+          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tb + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int tok = c0 + j;
+              if (real && tok < U.n && f < p.ff)
+                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(tanhf(__uint_as_float(v[j])));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[acc]);
+          else mbar_arrive_cluster(lead_tempty + 8 * acc);
+        }
+        if (real) {  // publish this warp's slice of H to phase-1 consumers on other SMs
+          __threadfence();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
+        }
+      } else {
+        // phase 1: split-K partial for 32 output columns -> slot[s]
+        const int r = tile * 128 + q * 32 + lane;
+        float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
+        for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tb + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < U.n && r < p.d) dst[static_cast<size_t>(c0 + j) * p.d] = __uint_as_float(v[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[acc]);
+          else mbar_arrive_cluster(lead_tempty + 8 * acc);
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's TMEM and barriers outlive every MMA / remote arrive
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
+  }
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_ffn_pair_t(const FfnParams& p, int sm_count, cudaStream_t s) {
+  constexpr size_t smem =
+      1024 + STAGES * (kTileA + BN * 64) + (2 * kMaxStages + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
+  static int configured_device = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_device != dev) {
+    cudaError_t e = cudaFuncSetAttribute(ffn_pair_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured_device = dev;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sm_count & ~1);
+  cfg.blockDim = dim3(kFfnThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, ffn_pair_kernel<BN, STAGES>, p);
+}
+
+// The CTA pair halves each SM's activation tiles but couples two SMs per
+// stage.  Measured on B200 (K3, CUDA events): it wins once the segments are
+// wide -- Mixtral-8x22B at T=256 (~128 rows per used expert) 638 -> 520 us,
+// T=128 (~64 rows) 478 -> 437 us, Mixtral-8x7B without Lynx at T=256 (~64
+// rows) 549 -> 515 us -- and loses on narrow ones (T=128 without Lynx, ~32
+// rows: 468 -> 474 us; DeepSeek-MoE C4, ~37 rows: 76.5 -> 83.2 us).  The host
+// only knows the expected rows per used expert, so that picks the kernel.
+// LYNX_FFN_PAIR=0/1 forces either kernel (A/B switch); unset or "auto": by rows.
+static bool use_pair(int bn, int rows_hint) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("LYNX_FFN_PAIR");
+    force = (e && e[0] == '0' && !e[1]) ? 0 : (e && e[0] == '1' && !e[1]) ? 1 : -1;
+  }
+  if (bn < 128) return false;  // T <= 64: decode batches stay on the single-CTA kernel
+  if (force >= 0) return force == 1;
+  return rows_hint >= 64;
+}
+
 template <int BN, int STAGES>
 static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s) {
   constexpr size_t smem =
@@ -378,16 +731,17 @@ static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s
   return launch_pdl(ffn_kernel<BN, STAGES>, dim3(sm_count), dim3(kFfnThreads), smem, s, p);
 }
 
-cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s) {
+cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, cudaStream_t s) {
+  const bool pair = use_pair(bn, rows_hint);
   switch (bn) {
     case 32:
       return launch_ffn_t<32, 10>(p, sm_count, s);
     case 64:
       return launch_ffn_t<64, 8>(p, sm_count, s);
     case 128:
-      return launch_ffn_t<128, 6>(p, sm_count, s);
+      return pair ? launch_ffn_pair_t<128, 8>(p, sm_count, s) : launch_ffn_t<128, 6>(p, sm_count, s);
     default:
-      return launch_ffn_t<256, 4>(p, sm_count, s);
+      return pair ? launch_ffn_pair_t<256, 6>(p, sm_count, s) : launch_ffn_t<256, 4>(p, sm_count, s);
   }
 }
 

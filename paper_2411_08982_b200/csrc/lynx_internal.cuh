@@ -195,7 +195,8 @@ cudaError_t launch_topk(const double* vals, int T, int N, int k, int32_t* ids, d
 cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_policy_t& w, double* counts,
                         cudaStream_t s);
 cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s);
-cudaError_t launch_ffn(const FfnParams& p, int bn, int sm_count, cudaStream_t s);
+// rows_hint: expected token rows per used expert (picks the CTA-pair kernel for wide segments)
+cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, cudaStream_t s);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s);
 cudaError_t launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,
                             cudaStream_t s);

@@ -403,3 +403,21 @@ def test_layer_at_maximum_sizes_vs_oracle(T, N, k, S, mode):
     ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights,
                            round_h_bf16=True, shared=range(N, N + S))
     assert O.norm_rel_err(_np(y), ref) <= TOL
+
+
+def test_cta_pair_kernel_forced_on_every_shape():
+    """K3's CTA-pair kernel (tcgen05 cta_group::2) normally runs only for wide
+    segments; force it (LYNX_FFN_PAIR=1) and rerun the layer parity tests so
+    narrow, odd-tile and shared-expert shapes go through it too (and =0 for
+    the single-CTA kernel on the wide shapes)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for force in ("1", "0"):
+        env = dict(os.environ, LYNX_FFN_PAIR=force)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                            os.path.join(here, "test_gpu_ffn.py"), "-k",
+                            "random_layer or maximum_sizes or shared_experts or deepseek or swiglu_vs_oracle"],
+                           env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, (force, r.stdout[-3000:], r.stderr[-2000:])
