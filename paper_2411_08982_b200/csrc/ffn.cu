@@ -737,11 +737,11 @@ cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, 
     case 32:
       return launch_ffn_t<32, 10>(p, sm_count, s);
     case 64:
-      return launch_ffn_t<64, 8>(p, sm_count, s);
+      return launch_ffn_t<64, 9>(p, sm_count, s);
     case 128:
-      return pair ? launch_ffn_pair_t<128, 8>(p, sm_count, s) : launch_ffn_t<128, 6>(p, sm_count, s);
+      return pair ? launch_ffn_pair_t<128, 9>(p, sm_count, s) : launch_ffn_t<128, 7>(p, sm_count, s);
     default:
-      return pair ? launch_ffn_pair_t<256, 6>(p, sm_count, s) : launch_ffn_t<256, 4>(p, sm_count, s);
+      return pair ? launch_ffn_pair_t<256, 7>(p, sm_count, s) : launch_ffn_t<256, 4>(p, sm_count, s);
   }
 }
 
