@@ -118,6 +118,62 @@ __device__ __forceinline__ void trace(int role, int id, uint64_t t0, uint64_t t1
 #define LYNX_TRACE_REC(role, id) (void)0
 #endif
 
+// Epilogue stores of one unit: this warp's 32 TMEM lanes (weight rows of
+// 128-row tile `tile`) x the segment's tokens.  Phase 0 applies the
+// activation and writes H (bf16); phase 1 writes the split-K partial (f32).
+// `real` = false masks the stores of a padding tile (CTA-pair kernel).
+__device__ __forceinline__ void epilogue_store(const FfnParams& p, const Unit& U, int tile, bool real, int q, int lane,
+                                               uint32_t tb) {
+  if (U.phase == 0) {
+    __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(p.h);
+    if (p.act == LYNX_ACT_SWIGLU) {
+      // lanes 0-15: gate rows, lanes 16-31: up rows of the same 16 features
+      const int f = tile * 64 + q * 16 + (lane & 15);
+      const bool upper = lane >= 16;
+      for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tb + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float send = __uint_as_float(upper ? v[j] : v[8 + j]);
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+          const float g = upper ? recv : __uint_as_float(v[j]);
+          const float uu = upper ? __uint_as_float(v[8 + j]) : recv;
+          const int tok = c0 + (upper ? 8 : 0) + j;
+          if (real && tok < U.n && f < p.ff)
+            H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(silu_mul(g, uu));
+        }
+      }
+    } else {
+      const int f = tile * 128 + q * 32 + lane;
+      for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tb + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int tok = c0 + j;
+          if (real && tok < U.n && f < p.ff)
+            H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(tanhf(__uint_as_float(v[j])));
+        }
+      }
+    }
+  } else {
+    // phase 1: split-K partial for 32 output columns -> slot[s]
+    const int r = tile * 128 + q * 32 + lane;
+    float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
+    for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tb + c0, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < U.n && r < p.d) dst[static_cast<size_t>(c0 + j) * p.d] = __uint_as_float(v[j]);
+    }
+  }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_constant__ FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -287,64 +343,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       LYNX_TRACE_T0;
       tc_fence_after();
       const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      epilogue_store(p, U, U.mt, true, q, lane, tb);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (U.phase == 0) {
-        __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(p.h);
-        if (p.act == LYNX_ACT_SWIGLU) {
-          // lanes 0-15: gate rows, lanes 16-31: up rows of the same 16 features
-          const int f = U.mt * 64 + q * 16 + (lane & 15);
-          const bool upper = lane >= 16;
-          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
-            uint32_t v[16];
-            tmem_ld16(tb + c0, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float send = __uint_as_float(upper ? v[j] : v[8 + j]);
-              const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-              const float g = upper ? recv : __uint_as_float(v[j]);
-              const float uu = upper ? __uint_as_float(v[8 + j]) : recv;
-              const int tok = c0 + (upper ? 8 : 0) + j;
-              if (tok < U.n && f < p.ff)
-                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(silu_mul(g, uu));
-            }
-          }
-        } else {
-          const int f = U.mt * 128 + q * 32 + lane;
-          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
-            uint32_t v[16];
-            tmem_ld16(tb + c0, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int tok = c0 + j;
-              if (tok < U.n && f < p.ff)
-                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(tanhf(__uint_as_float(v[j])));
-            }
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
         // publish this warp's slice of H to phase-1 consumers on other SMs
         __threadfence();
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
-      } else {
-        // phase 1: split-K partial for 32 output columns -> slot[s]
-        const int r = U.mt * 128 + q * 32 + lane;
-        float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
-        for (int c0 = 0; c0 < U.nmma; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(tb + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < U.n && r < p.d) dst[static_cast<size_t>(c0 + j) * p.d] = __uint_as_float(v[j]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
       if (lane == 0) LYNX_TRACE_REC(2, u);
       acc ^= 1;
@@ -585,71 +593,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
       tc_fence_after();
       const int tile = 2 * U.mt + static_cast<int>(rank);
       const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
-      if (U.phase == 0) {
-        const bool real = tile < p.tiles1;  // the second tile of an odd count is padding
-        __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(p.h);
-        if (p.act == LYNX_ACT_SWIGLU) {
-          const int f = tile * 64 + q * 16 + (lane & 15);
-          const bool upper = lane >= 16;
-          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
-            uint32_t v[16];
-            tmem_ld16(tb + c0, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float send = __uint_as_float(upper ? v[j] : v[8 + j]);
-              const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-              const float g = upper ? recv : __uint_as_float(v[j]);
-              const float uu = upper ? __uint_as_float(v[8 + j]) : recv;
-              const int tok = c0 + (upper ? 8 : 0) + j;
-              if (real && tok < U.n && f < p.ff)
-                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(silu_mul(g, uu));
-            }
-          }
-        } else {
-          const int f = tile * 128 + q * 32 + lane;
-          for (int c0 = 0; c0 < U.nmma; c0 += 16) {
-            uint32_t v[16];
-            tmem_ld16(tb + c0, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int tok = c0 + j;
-              if (real && tok < U.n && f < p.ff)
-                H[static_cast<size_t>(U.row0 + tok) * p.ff + f] = __float2bfloat16_rn(tanhf(__uint_as_float(v[j])));
-            }
-          }
-        }
-        tc_fence_before();
+      const bool real = tile < (U.phase == 0 ? p.tiles1 : p.tiles2);  // the second tile of an odd count is padding
+      epilogue_store(p, U, tile, real, q, lane, tb);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_cluster(lead_tempty + 8 * acc);
+      }
+      if (U.phase == 0 && real) {  // publish this warp's slice of H to phase-1 consumers on other SMs
+        __threadfence();
+        fence_proxy_async();
         __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(&tempty[acc]);
-          else mbar_arrive_cluster(lead_tempty + 8 * acc);
-        }
-        if (real) {  // publish this warp's slice of H to phase-1 consumers on other SMs
-          __threadfence();
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
-        }
-      } else {
-        // phase 1: split-K partial for 32 output columns -> slot[s]
-        const int r = tile * 128 + q * 32 + lane;
-        float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
-        for (int c0 = 0; c0 < U.nmma; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(tb + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < U.n && r < p.d) dst[static_cast<size_t>(c0 + j) * p.d] = __uint_as_float(v[j]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(&tempty[acc]);
-          else mbar_arrive_cluster(lead_tempty + 8 * acc);
-        }
+        if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
       }
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
