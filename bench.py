@@ -503,10 +503,10 @@ def run_ep_p2p(args, c, rank, world, local_rank):
         torch.cuda.synchronize()
         dist.barrier()
     steps = reps * n
-    ms = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda")
+    ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    crit = torch.tensor([statistics.mean(used_local)], device="cuda")
+    crit = torch.tensor([float(statistics.mean(used_local))], dtype=torch.float64, device="cuda")  # same dtype on every rank
     tot = crit.clone()
     dist.all_reduce(crit, op=dist.ReduceOp.MAX)
     dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -524,7 +524,7 @@ def run_ep_p2p(args, c, rank, world, local_rank):
         o_host.copy_(outs[l], non_blocking=True)
     c1.record()
     torch.cuda.synchronize()
-    me = torch.tensor([c0.elapsed_time(c1) / steps], device="cuda")
+    me = torch.tensor([c0.elapsed_time(c1) / steps], dtype=torch.float64, device="cuda")
     dist.all_reduce(me, op=dist.ReduceOp.MAX)
     ms_e2e = float(me.item())
     Tg = T * world
@@ -594,10 +594,10 @@ def run_ep(args, c, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    crit = torch.tensor([statistics.mean(used_local)], device="cuda")
+    crit = torch.tensor([float(statistics.mean(used_local))], dtype=torch.float64, device="cuda")  # same dtype on every rank
     tot = crit.clone()
     dist.all_reduce(crit, op=dist.ReduceOp.MAX)
     dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -616,7 +616,7 @@ def run_ep(args, c, rank, world, local_rank):
         o_host.copy_(out, non_blocking=True)
     c1.record()
     torch.cuda.synchronize()
-    me = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+    me = torch.tensor([c0.elapsed_time(c1) / args.steps], dtype=torch.float64, device="cuda")
     dist.all_reduce(me, op=dist.ReduceOp.MAX)
     ms_e2e = float(me.item())
     Tg = T * world

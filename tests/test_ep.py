@@ -223,3 +223,27 @@ def test_p2p_ep_two_processes_one_gpu():
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "rank 0: ok" in out.stdout and "rank 1: ok" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["c2", "c5"])
+def test_bench_multi_rank_path_runs(config):
+    """bench.py's N>1 path as the driver launches it (torchrun, one rank per
+    GPU), here with all four ranks sharing GPU 0 (--share-gpu, gloo): the
+    peer-memory EP step, the max-over-ranks timing and the e2e leg must run
+    to one JSON line.  Per-rank statistics differ between ranks, so every
+    collective must use one dtype on all ranks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "4",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--gpus", "4", "--share-gpu", "--config", config, "--steps", "4", "--warmup", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 4 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["parallelism"] == "ep4"
