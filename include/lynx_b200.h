@@ -328,6 +328,13 @@ typedef struct lynx_ep_peers {
   int32_t *epoch;
 } lynx_ep_peers_t;
 
+/* Let kernels on the calling thread's current device load/store memory of
+ * device `peer_device` (cudaDeviceEnablePeerAccess; already enabled or the
+ * same device: LYNX_OK; no P2P path: LYNX_ERR_UNSUPPORTED).  Peer buffers
+ * opened over CUDA IPC are mapped for the owner's device only, so every rank
+ * calls this for every other rank's device before the first layer. */
+int lynx_enable_peer_access(int peer_device);
+
 /* K0 on the local rows into logits_local rows rank*Tl.., then to every peer. */
 int lynx_ep_p2p_route(const uint16_t *router_wt, const uint16_t *hidden_local, int d, int N,
                       const lynx_ep_peers_t *peers, lynx_stream_t stream);

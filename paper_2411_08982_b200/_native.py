@@ -105,6 +105,7 @@ _SIGS = {
     "lynx_attention": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_advance_position": (_i, [_p, _i, _p]),
     "lynx_trace_append": (_i, [_p, _p, _i, _p, _p]),
+    "lynx_enable_peer_access": (_i, [_i]),
     "lynx_ep_p2p_route": (_i, [_p, _p, _i, _i, _p, _p]),
     "lynx_ep_p2p_dispatch": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p]),
     "lynx_ep_p2p_expert": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, ctypes.c_size_t, _p]),

@@ -746,6 +746,21 @@ int lynx_ep_combine(const uint16_t* hidden_local, const float* recv_partial, int
   return cuda_status(launch_ep_combine(hidden_local, recv_partial, T_local, G, d, out, stream));
 }
 
+int lynx_enable_peer_access(int peer_device) {
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return LYNX_ERR_CUDA;
+  if (peer_device == cur) return LYNX_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, cur, peer_device) != cudaSuccess) return LYNX_ERR_CUDA;
+  if (!can) return LYNX_ERR_UNSUPPORTED;
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free "already enabled" status
+    return LYNX_OK;
+  }
+  return cuda_status(e);
+}
+
 int lynx_ep_p2p_route(const uint16_t* router_wt, const uint16_t* hidden_local, int d, int N,
                       const lynx_ep_peers_t* peers, lynx_stream_t stream) {
   int st = check_peers(peers);

@@ -116,6 +116,11 @@ def ipc_peers(group, Tl: int, N: int, d: int) -> PeerSet:
     mine = {n: t.untyped_storage()._share_cuda_() for n, t in bufs.items()}
     allh = [None] * G
     dist.all_gather_object(allh, mine, group=group)
+    # Opened IPC allocations are mapped for their owner's device only; our
+    # kernels run on this rank's device and store into them over NVLink.
+    here = torch.cuda.current_device()
+    for dev in sorted({allh[r][n][0] for r in range(G) if r != rank for n in bufs} - {here}):
+        nat.check(nat.lib().lynx_enable_peer_access(int(dev)), "lynx_enable_peer_access")
     opened, arrays = [], {}
     for n, t in bufs.items():
         ptrs = []
