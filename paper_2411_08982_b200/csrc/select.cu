@@ -1010,6 +1010,23 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
         }
       }
     } else {  // apply_policy on a given selection
+      if (live && j < k) {
+        IDS[t * k + j] = a.ids[t * k + j];
+        PROBS[t * k + j] = a.probs[t * k + j];
+      }
+      // The confidence follows from the selection itself: top1 = the first
+      // pick's probability (the row max), margin = first - second pick
+      // (router.py:190-192).  The probability row is then never staged: the
+      // remap reads its retained entries straight from `full`.  A row routed
+      // from non-finite logits arrives with NaN probabilities.
+      if (a.pol.confidence_metric != LYNX_CONF_MARGIN || k >= 2) {
+        if (live && j == 0) {
+          const double p0 = a.probs[t * k], p1 = k > 1 ? a.probs[t * k + 1] : 0.0;
+          if (isnan(p0)) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
+          CONF[t] = a.pol.confidence_metric == LYNX_CONF_MARGIN ? p0 - p1 : p0;
+        }
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < EPL; ++q) {
         const int e = j + 8 * q;
@@ -1017,10 +1034,6 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
         if (live && e < N) P[static_cast<size_t>(t) * N + e] = v[q];
         // a row routed from non-finite logits arrives as NaN (router_route_kernel)
         if (live && e < N && isnan(v[q])) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
-      }
-      if (live && j < k) {
-        IDS[t * k + j] = a.ids[t * k + j];
-        PROBS[t * k + j] = a.probs[t * k + j];
       }
     }
     SEL_TS_LOCAL(13);
@@ -1081,7 +1094,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
       // rolled slot loop (one inlined arg-max): the kernel runs from a cold
       // instruction cache once per layer, so code size is latency.  Slot
       // probabilities park in WT until the row's renormalisation.
-      const double* prow = P + static_cast<size_t>(t) * N;
+      const double* prow = (kGiven ? a.full : P) + static_cast<size_t>(t) * N;
       if (EPL > 4 && nR <= 32)
         remap_row<(EPL > 4 ? 4 : EPL)>(prow, live, t, k, j, keep, nR, s_rlist, IDS, PROBS, ASG, WT);
       else
@@ -1348,7 +1361,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
     lane_mark(taken, b, j);
     if (live && j == 0) {
       ids[t * k + r] = b;
-      probs[t * k + r] = bv;
+      probs[t * k + r] = bad ? NAN : bv;
     }
   }
 }
