@@ -874,39 +874,46 @@ __device__ __forceinline__ void remap_row(const double* prow, bool live, int t, 
     v[q] = (live && c < nR) ? prow[rlist[c]] : 0.0;
   }
   const uint32_t all_c = lane_bits<EPR>(nR >= 64 ? ~0ull : ((1ull << nR) - 1ull), j);
-  uint32_t occ = 0;  // lane-local: retained original choices (compact indices)
+  // Retained originals keep their slot and are occupied up front; the
+  // displaced slots, in slot order, take the best unoccupied retained experts
+  // in (p desc, c asc) order -- so one arg-max round per displaced slot of
+  // the warp's neediest token, not one per slot -- or collapse onto the best
+  // retained expert when none is left.
+  uint32_t occ = 0, dmask = 0;  // occ: lane-local compact bits; dmask: displaced slots
 #pragma unroll 1
   for (int r = 0; r < k; ++r) {
     const int e = live ? IDS[t * k + r] : 0;
-    if ((keep >> e) & 1ull) lane_mark(occ, __popcll(keep & ((1ull << e) - 1ull)), j);
-  }
-#pragma unroll 1
-  for (int r = 0; r < k; ++r) {
-    int e = live ? IDS[t * k + r] : 0;
-    const bool disp = !((keep >> e) & 1ull);
-    double val = live ? PROBS[t * k + r] : 0.0;  // p[e] of a kept original (same bits as v)
-    // the arg-max runs only when some group of the warp has slot r displaced
-    // (warp-uniform, so the shuffles stay converged)
-    if (__any_sync(kFull, live && disp)) {
-      double bv;
-      int pick = grp_best<EPR>(v, all_c & ~occ, j, &bv);
-      if (__any_sync(kFull, pick < 0)) {
-        double bv_any;
-        const int any = grp_best<EPR>(v, all_c, j, &bv_any);  // collapse (policy.py:197-200)
-        if (pick < 0) {
-          pick = any;
-          bv = bv_any;
-        }
-      }
-      if (disp) {
-        if (pick >= 0) lane_mark(occ, pick, j);
-        e = pick >= 0 ? rlist[pick] : -1;
-        val = bv;
-      }
-    }
+    if ((keep >> e) & 1ull)
+      lane_mark(occ, __popcll(keep & ((1ull << e) - 1ull)), j);
+    else
+      dmask |= 1u << r;
     if (live && j == 0) {
       ASG[t * k + r] = e;
-      WT[t * k + r] = val;
+      WT[t * k + r] = PROBS[t * k + r];  // p[e] of the original (same bits as the row)
+    }
+  }
+  const int d = live ? __popc(dmask) : 0;
+  const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(d));  // warp-uniform: shuffles stay converged
+#pragma unroll 1
+  for (int i = 0; i < rounds; ++i) {
+    double bv;
+    int pick = grp_best<EPR>(v, all_c & ~occ, j, &bv);
+    if (__any_sync(kFull, pick < 0)) {
+      double bv_any;
+      const int any = grp_best<EPR>(v, all_c, j, &bv_any);  // collapse (policy.py:197-200)
+      if (pick < 0) {
+        pick = any;
+        bv = bv_any;
+      }
+    }
+    if (i < d) {
+      if (pick >= 0) lane_mark(occ, pick, j);
+      const int r = __ffs(dmask) - 1;
+      dmask &= dmask - 1;
+      if (j == 0) {
+        ASG[t * k + r] = pick >= 0 ? rlist[pick] : -1;
+        WT[t * k + r] = bv;
+      }
     }
   }
 }
