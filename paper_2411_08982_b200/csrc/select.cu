@@ -710,42 +710,46 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
   if (active) {
     double slot_p[LYNX_MAX_TOPK];
     int asg[LYNX_MAX_TOPK];
+    // slot loops unrolled over LYNX_MAX_TOPK: the per-slot arrays stay in
+    // registers (a rolled loop with a run-time slot index puts them on the stack)
     if (run_policy) {
       const uint64_t keep = s_keepmask;
       uint64_t occupied = 0;
-#pragma unroll 1
-      for (int r = 0; r < k; ++r)
-        if ((keep >> ids[r]) & 1ull) occupied |= 1ull << ids[r];
-#pragma unroll 1
-      for (int r = 0; r < k; ++r) {
-          int e = ids[r];
-          if (!((keep >> e) & 1ull)) {
-            int pick = reg_best<NT>(p, keep & ~occupied);
-            if (pick < 0) pick = reg_best<NT>(p, keep);  // collapse (policy.py:197-200)
-            e = pick;
-            occupied |= 1ull << e;
-          }
-          asg[r] = e;
-          slot_p[r] = reg_at<NT>(p, e);
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r)
+        if (r < k && ((keep >> ids[r]) & 1ull)) occupied |= 1ull << ids[r];
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+        if (r >= k) break;
+        int e = ids[r];
+        if (!((keep >> e) & 1ull)) {
+          int pick = reg_best<NT>(p, keep & ~occupied);
+          if (pick < 0) pick = reg_best<NT>(p, keep);  // collapse (policy.py:197-200)
+          e = pick;
+          occupied |= 1ull << e;
         }
+        asg[r] = e;
+        slot_p[r] = reg_at<NT>(p, e);
+      }
     } else {
-#pragma unroll 1
-      for (int r = 0; r < k; ++r) {
-          asg[r] = ids[r];
-          slot_p[r] = probs[r];
-        }
+#pragma unroll
+      for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+        asg[r] = r < k ? ids[r] : 0;
+        slot_p[r] = r < k ? probs[r] : 0.0;
+      }
     }
     const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot_p, k);
     if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);
     const double inv = 1.0 / total;
-#pragma unroll 1
-    for (int r = 0; r < k; ++r) {
-        const double w = slot_p[r] * inv;
-        ASG[t * k + r] = asg[r];
-        WT[t * k + r] = w;
-        a.assigned[t * k + r] = asg[r];
-        a.weights[t * k + r] = w;
-      }
+#pragma unroll
+    for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+      if (r >= k) break;
+      const double w = slot_p[r] * inv;
+      ASG[t * k + r] = asg[r];
+      WT[t * k + r] = w;
+      a.assigned[t * k + r] = asg[r];
+      a.weights[t * k + r] = w;
+    }
     a.conf[t] = CONF[t];
     if (a.important) a.important[t] = accuracy ? IMP[t] : 0;
   }
