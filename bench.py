@@ -10,12 +10,19 @@ combine + residual (K4).  Default workload (configs[1]): Mixtral-8x7B layer
 shape, d=4096, ff=14336, 8 experts, top-2, bf16, decode batch 32, Lynx
 latency policy dropping 4 experts.
 
-N > 1 (torchrun): expert parallel, rank g owns 8/N experts, 32 tokens per
-rank (weak scaling), NCCL all-gather of logits + all-to-all dispatch/combine.
+N > 1: expert parallel, rank g owns N_experts/N experts.  The config's batch
+is the GLOBAL batch (fixed as N grows, scaling "strong"; T/N rows per rank);
+--scaling weak keeps T rows per rank instead.  The exchanges run over NVLink
+peer memory inside the producing kernels (--ep-transport p2p, the product
+path) or as NCCL all-gather + all-to-all (--ep-transport nccl, the baseline).
+Without torchrun, --gpus N re-launches itself through torch.distributed.run
+with N local ranks (127.0.0.1).
 
 --impl reference: the reference's CPU algorithm (the oracle port of moetrim's
 route_batch + apply_policy + forward_layer with a SwiGLU expert, numpy/BLAS
-on all host cores) on the same workload; rank 0 only.
+on all host cores) on the same workload; rank 0 only.  Both arms also time
+the reference as shipped -- the same calls with its own float64
+tanh(x w1) w2 expert (simulator.py:77-113) -- as cpu_baseline_f64_tanh2.
 """
 
 from __future__ import annotations
@@ -48,9 +55,12 @@ CONFIGS = {
     # configs[3]: DeepSeek-MoE-16B shape, 64 routed + 2 shared experts, top-6, dynamic (accuracy) selection
     "c4": dict(workload="deepseek-moe-16b-layer-decode-bs128-lynx-accuracy-budget16", d=2048, ff=1408, N=64, S=2,
                k=6, T=128, mode="accuracy", drop=0, budget=16, rotate=6),
-    # configs[4]: Mixtral-8x22B expert-parallel shape (T is per rank)
-    "c5": dict(workload="mixtral-8x22b-moe-layer-decode-lynx-latency-drop4", d=6144, ff=16384, N=8, k=2, T=32,
-               mode="latency", drop=4, rotate=3),
+    # configs[4]: Mixtral-8x22B shape, decode batch 256 (the global batch: T/G rows per rank under EP)
+    "c5": dict(workload="mixtral-8x22b-moe-layer-decode-bs256-lynx-latency-drop4", d=6144, ff=16384, N=8, k=2,
+               T=256, mode="latency", drop=4, rotate=3),
+    # the same layer at 32 tokens (C5's per-GPU batch at EP8)
+    "c5-bs32": dict(workload="mixtral-8x22b-moe-layer-decode-bs32-lynx-latency-drop4", d=6144, ff=16384, N=8, k=2,
+                    T=32, mode="latency", drop=4, rotate=3),
 }
 
 SWIGLU_BYTES = lambda c: 3 * c["d"] * c["ff"] * 2  # noqa: E731
@@ -169,6 +179,67 @@ def cpu_layer_step(st, i):
     return O.forward_swiglu(h, st["w1"], st["w3"], st["w2"], m.assigned, m.weights, shared=st["shared"])
 
 
+def cpu_tanh2_setup(c, seed=0):
+    """The reference as shipped (simulator.py:77-113): float64 router, route_batch,
+    apply_policy and forward_layer with its tanh(x @ w1) @ w2 expert; weights
+    [d, ff] / [ff, d] float64 of the experts the sampled batches use."""
+    import numpy as np
+
+    from oracle import lynx_oracle as O
+    rng = np.random.default_rng(seed)
+    T, d, ff, N, k = c["T"], c["d"], c["ff"], c["N"], c["k"]
+    router_w = rng.standard_normal((d, N)) * (2.0 / np.sqrt(d))
+    batches = [rng.standard_normal((T, d)) for _ in range(2)]
+    pol = O.Policy(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
+    used = set()
+    for h in batches:
+        ids, probs, full = O.route(O.router_logits(h, router_w), k)
+        used.update(int(e) for e in np.unique(O.apply(ids, probs, full, pol).assigned))
+    w1, w2 = {}, {}
+    for e in sorted(used):
+        w1[e] = rng.standard_normal((d, ff), dtype=np.float32).astype(np.float64) / np.sqrt(d)
+        w2[e] = rng.standard_normal((ff, d), dtype=np.float32).astype(np.float64) / np.sqrt(ff)
+    return dict(router_w=router_w, batches=batches, pol=pol, w1=w1, w2=w2, k=k)
+
+
+def cpu_tanh2_step(st, i):
+    from oracle import lynx_oracle as O
+    h = st["batches"][i % len(st["batches"])]
+    ids, probs, full = O.route(O.router_logits(h, st["router_w"]), st["k"])
+    m = O.apply(ids, probs, full, st["pol"])
+    return O.forward_tanh2(h, st["w1"], st["w2"], m.assigned, m.weights)
+
+
+def cpu_baseline_tanh2(c, steps=2):
+    if c.get("S", 0):
+        return {"skipped": "the reference has no shared experts (DeepSeek-MoE extension)"}
+    st = cpu_tanh2_setup(c)
+    cpu_tanh2_step(st, 0)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        cpu_tanh2_step(st, i)
+    nl = c.get("layers", 1)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": c["T"] / (dt * nl), "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+            "ms_per_step": dt * 1e3 * nl,
+            "sample": f"{steps} layer steps (T={c['T']}) of the reference as shipped: float64 router, route_batch, "
+                      f"apply_policy, forward_layer with tanh(x w1) w2 experts (simulator.py:77-113) restated in "
+                      f"oracle/lynx_oracle.py, numpy/OpenBLAS" + (f"; x {nl} layers" if nl > 1 else "")}
+
+
+def config_dict(c, world=1, scaling="strong"):
+    """The workload description, identical in both arms (no run-specific data)."""
+    T = c["T"]
+    per_gpu = T // world if scaling == "strong" else T
+    out = {"workload": c["workload"], "d_model": c["d"], "d_ff": c["ff"], "experts": c["N"], "top_k": c["k"],
+           "shared_experts": c.get("S", 0), "global_batch": per_gpu * world, "tokens_per_gpu": per_gpu,
+           "policy": policy_name(c), "parallelism": "single" if world == 1 else f"ep{world}",
+           "scaling": scaling}
+    if "layers" in c:
+        out.update(layers=c["layers"], prefill_len=c["prefill"], d_head=c["d_head"])
+    return out
+
+
 def policy_name(c):
     if c["mode"] == "accuracy":
         return f"accuracy tau 0.5 sample 8 budget {c.get('budget', 4)}"
@@ -211,15 +282,16 @@ def run_reference(args, c):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": c["workload"], "d_model": c["d"], "d_ff": c["ff"], "experts": c["N"],
-                   "top_k": c["k"], "tokens": c["T"], "policy": policy_name(c),
-                   "parallelism": "host"},
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(c, args.gpus, args.scaling),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": "each step = one full layer step of the oracle port (moetrim's "
-                                   "route_batch/apply_policy/forward_layer restated, SwiGLU fp32)"},
+                         "sample": f"each step = one full layer step (global batch T={c['T']}) of the oracle port "
+                                   "(moetrim's route_batch/apply_policy/forward_layer restated, SwiGLU fp32), "
+                                   "numpy/OpenBLAS on every host core"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline_f64_tanh2"] = cpu_baseline_tanh2(c)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -243,6 +315,7 @@ def run_single(args, c):
         layers[i % n](hid[i % n], outs[i % n])
     torch.cuda.synchronize()
     used = [layers[l].used_experts() for l in range(n)]
+    ffn_kernel = layers[0].ffn_kernel()
 
     # CUDA graphs: all rotating layer copies captured back to back in ONE
     # graph (a deployment runs its layers inside one graph, so no graph
@@ -335,17 +408,15 @@ def run_single(args, c):
     result = {
         "metric": METRIC, "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
-        "config": {"workload": c["workload"], "d_model": d, "d_ff": ff, "experts": N, "top_k": k,
-                   "global_batch": T, "tokens_per_gpu": T, "policy": policy_name(c),
-                   "parallelism": "single", "weight_copies": n,
-                   "graph": f"{n} layer calls (one per rotating weight copy) per CUDA-graph replay",
-                   "shared_experts": c.get("S", 0),
-                   "l2": f"inputs > L2: {n} rotating layer copies "
-                         f"({n * (N + c.get('S', 0)) * SWIGLU_BYTES(c) / 1e9:.1f} GB) >> 126 MB L2",
-                   "used_experts_per_copy": used, "mean_used_experts": mean_used},
-        "roofline": {"bound": "hbm", "kernel": "ffn_kernel (K3, tcgen05 grouped SwiGLU)",
+        "config": config_dict(c),
+        "run": {"weight_copies": n,
+                "graph": f"{n} layer calls (one per rotating weight copy) per CUDA-graph replay",
+                "l2": f"inputs > L2: {n} rotating layer copies "
+                      f"({n * (N + c.get('S', 0)) * SWIGLU_BYTES(c) / 1e9:.1f} GB) >> 126 MB L2",
+                "used_experts_per_copy": used, "mean_used_experts": mean_used, "ffn_kernel": ffn_kernel},
+        "roofline": {"bound": "hbm", "kernel": f"{ffn_kernel} (K3, tcgen05 grouped SwiGLU)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src,
                      "frac_of_8TBs": achieved / 8000.0,
@@ -429,13 +500,11 @@ def run_stack(args, c):
     return {
         "metric": METRIC, "value": best["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": best["ms_per_step"], "us_per_step": best["ms_per_step"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: random-init Mixtral-shaped bf16 weights (32 layers, 90 GB), N(0,1) prefill inputs",
-        "config": {"workload": c["workload"], "d_model": d, "d_ff": ff, "experts": N, "top_k": k, "layers": nl,
-                   "global_batch": B, "tokens_per_gpu": B, "policy": f"latency drop {c['drop']} (budget "
-                   f"{N - c['drop']})", "parallelism": "single", "prefill_len": P, "d_head": c["d_head"],
-                   "l2": "inputs > L2: each step streams every layer's used experts (>= 45 GB) >> 126 MB L2",
-                   "budget_sweep": sweep},
+        "config": config_dict(c),
+        "run": {"l2": "inputs > L2: each step streams every layer's used experts (>= 45 GB) >> 126 MB L2",
+                "kept_budget": N - c["drop"], "budget_sweep": sweep},
         "roofline": {"bound": "hbm", "kernel": "whole decode step (32 x [attention + fused router, K1..K4])",
                      "achieved": best["achieved_gbs"], "peak": peak, "unit": "GB/s",
                      "frac": best["achieved_gbs"] / peak, "peak_source": peak_src,
@@ -449,7 +518,53 @@ def run_stack(args, c):
     }
 
 
-def run_ep_p2p(args, c, rank, world, local_rank):
+def _ep_stats(used_local, world, c, ms, phase_ms, phase_names):
+    """Per-rank / critical-path / aggregate expert bytes and the phase split, reduced over ranks."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    mine = torch.tensor([float(statistics.mean(used_local))], dtype=torch.float64, device=dev)
+    per_rank = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(per_rank, mine)
+    used = [float(t.item()) for t in per_rank]
+    ph = torch.tensor(phase_ms, dtype=torch.float64, device=dev)
+    dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    eb = SWIGLU_BYTES(c)
+    return {
+        "used_experts_per_rank": used,
+        "expert_bytes_per_rank": [u * eb for u in used],
+        "critical_path_bytes": max(used) * eb,
+        "aggregate_bytes": sum(used) * eb,
+        "phase_ms_max_over_ranks": dict(zip(phase_names, [float(x) for x in ph.tolist()])),
+    }
+
+
+def _ep_result(args, c, world, Tl, ms, ms_e2e, stats, transport, kernel_note, launches, clocks):
+    peak, peak_src = measured_peaks()
+    crit = stats["critical_path_bytes"]
+    Tg = Tl * world
+    return {
+        "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
+        "config": config_dict(c, world, args.scaling),
+        "run": dict(stats, transport=transport, weight_copies=c["rotate"]),
+        "roofline": {"bound": "hbm", "kernel": kernel_note,
+                     "achieved": crit / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": crit / (ms * 1e-3) / 1e9 / peak, "peak_source": peak_src,
+                     "note": "critical-path expert bytes (max over ranks) / whole step time, exchanges included",
+                     "aggregate_achieved_gbs": stats["aggregate_bytes"] / (ms * 1e-3) / 1e9,
+                     "traffic": None},
+        "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": Tl * c["d"] * 2, "d2h_bytes_per_step": Tl * c["d"] * 2,
+                "note": "per rank: its T/G input rows in, its output rows out"},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks.summary(),
+    }
+
+
+def run_ep_p2p(args, c, rank, world, local_rank, peers):
     """Expert parallel over NVLink peer memory (ep_p2p.P2PEPLayer): the logits
     all-gather, dispatch and return are stores issued by the producing
     kernels into the peers' CUDA-IPC-shared buffers; one CUDA graph per step."""
@@ -459,10 +574,8 @@ def run_ep_p2p(args, c, rank, world, local_rank):
     import paper_2411_08982_b200 as L
     from paper_2411_08982_b200 import ep as EP
     from paper_2411_08982_b200 import ep_p2p as P2P
-    T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
-    if N % world:
-        raise SystemExit(f"{N} experts do not shard over {world} GPUs")
-    peers = P2P.ipc_peers(dist.group.WORLD, T, N, d)
+    Tl = c["T"] // world if args.scaling == "strong" else c["T"]
+    d, ff, N, k, n = c["d"], c["ff"], c["N"], c["k"], c["rotate"]
     spec = L.MoEModelSpec(num_layers=1, num_experts=N, top_k=k, d_model=d, d_ff=ff)
     pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
     layers = []
@@ -473,7 +586,7 @@ def run_ep_p2p(args, c, rank, world, local_rank):
         del full
         torch.cuda.empty_cache()
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    hid = [torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
+    hid = [torch.randn((Tl, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
     outs = [torch.empty_like(h) for h in hid]
     for i in range(max(args.warmup, n)):
         layers[i % n](hid[i % n], outs[i % n])
@@ -483,6 +596,24 @@ def run_ep_p2p(args, c, rank, world, local_rank):
     for l in range(n):
         a = layers[l].assigned_local
         used_local.append(int((torch.bincount(a[a >= 0].long(), minlength=N // world) > 0).sum()))
+    # phase split (eager, events between the four calls; serialises the programmatic launches)
+    names = ["route", "dispatch", "expert", "combine"]
+    reps = min(20, args.steps)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(reps)]
+    dist.barrier()
+    for i in range(reps):
+        lay, h = layers[i % n], hid[i % n]
+        evs[i][0].record()
+        lay.route(h)
+        evs[i][1].record()
+        lay.dispatch(h)
+        evs[i][2].record()
+        lay.expert()
+        evs[i][3].record()
+        lay.combine(h, outs[i % n])
+        evs[i][4].record()
+    torch.cuda.synchronize()
+    phase = [statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(reps)) for j in range(4)]
     g_all = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_all):
         for l in range(n):
@@ -503,16 +634,11 @@ def run_ep_p2p(args, c, rank, world, local_rank):
         torch.cuda.synchronize()
         dist.barrier()
     steps = reps * n
-    ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    crit = torch.tensor([float(statistics.mean(used_local))], dtype=torch.float64, device="cuda")  # same dtype on every rank
-    tot = crit.clone()
-    dist.all_reduce(crit, op=dist.ReduceOp.MAX)
-    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    # e2e: pinned host input/output per step around the same graphed layers
+    ms = _max_over_ranks(e0.elapsed_time(e1) / steps)
+    stats = _ep_stats(used_local, world, c, ms, phase, names)
+    # e2e: pinned host input/output per step around the same layers
     h_host = [h.cpu().pin_memory() for h in hid]
-    o_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+    o_host = torch.empty((Tl, d), dtype=torch.bfloat16).pin_memory()
     dist.barrier()
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -524,46 +650,36 @@ def run_ep_p2p(args, c, rank, world, local_rank):
         o_host.copy_(outs[l], non_blocking=True)
     c1.record()
     torch.cuda.synchronize()
-    me = torch.tensor([c0.elapsed_time(c1) / steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(me, op=dist.ReduceOp.MAX)
-    ms_e2e = float(me.item())
-    Tg = T * world
-    peak, peak_src = measured_peaks()
-    crit_bytes = float(crit.item()) * SWIGLU_BYTES(c)
-    return {
-        "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
-        "config": {"workload": c["workload"] + f"-ep{world}", "d_model": d, "d_ff": ff, "experts": N,
-                   "top_k": k, "global_batch": Tg, "tokens_per_gpu": T, "policy": policy_name(c),
-                   "parallelism": f"ep{world}", "transport": "nvlink peer memory (lynx_ep_p2p_*, CUDA-IPC shared buffers)",
-                   "weight_copies": n, "mean_used_experts_total": float(tot.item()),
-                   "critical_path_used_experts": float(crit.item())},
-        "roofline": {"bound": "hbm", "kernel": "ffn_kernel per rank (critical path)",
-                     "achieved": crit_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": crit_bytes / (ms * 1e-3) / 1e9 / peak, "peak_source": peak_src,
-                     "note": "critical-path bytes / whole step time (includes the peer-memory exchanges)",
-                     "traffic": None},
-        "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
-                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
-        "gpu_launches": 11 * steps,
-        "clocks": clocks.summary(),
-    }
+    ms_e2e = _max_over_ranks(c0.elapsed_time(c1) / steps)
+    args.steps = steps
+    return _ep_result(args, c, world, Tl, ms, ms_e2e, stats,
+                      "nvlink peer memory (lynx_ep_p2p_*, CUDA-IPC shared buffers; stores issued by K0 / the "
+                      "dispatch kernel / K4, release-acquire flags)",
+                      "ffn_kernel per rank (critical path)", 11, clocks)
+
+
+def _max_over_ranks(v):
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_ep(args, c, rank, world, local_rank):
+    """Expert parallel with NCCL collectives (ep.ep_layer): all-gather of the
+    logits, all-to-all dispatch and return around the same kernels."""
     import torch
     import torch.distributed as dist
 
     import paper_2411_08982_b200 as L
     from paper_2411_08982_b200 import ep as EP
-    T, d, ff, N, k, n = c["T"], c["d"], c["ff"], c["N"], c["k"], c["rotate"]
-    if N % world:
-        raise SystemExit(f"{N} experts do not shard over {world} GPUs")
-    shape = EP.EPShape(num_experts=N, top_k=k, d_model=d, d_ff=ff, tokens_per_rank=T, world_size=world, rank=rank)
+    Tl = c["T"] // world if args.scaling == "strong" else c["T"]
+    d, ff, N, k, n = c["d"], c["ff"], c["N"], c["k"], c["rotate"]
+    shape = EP.EPShape(num_experts=N, top_k=k, d_model=d, d_ff=ff, tokens_per_rank=Tl, world_size=world, rank=rank)
     spec = L.MoEModelSpec(num_layers=1, num_experts=N, top_k=k, d_model=d, d_ff=ff)
-    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"])
+    pol = L.PolicyConfig(mode=c["mode"], drop_count=c["drop"], freq_keep_budget=c.get("budget", 4))
     ops = []
     for l in range(n):
         full = L.build_swiglu_model(spec, seed=100 + l)  # same seed on every rank -> identical model
@@ -573,7 +689,7 @@ def run_ep(args, c, rank, world, local_rank):
         del full
         torch.cuda.empty_cache()
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    hid = [torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
+    hid = [torch.randn((Tl, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
     for i in range(max(args.warmup, n)):
         EP.ep_layer(shape, ops[i % n], hid[i % n])
     torch.cuda.synchronize()
@@ -582,6 +698,16 @@ def run_ep(args, c, rank, world, local_rank):
         EP.ep_layer(shape, ops[l], hid[l])
         a = ops[l].assigned_local
         used_local.append(int((torch.bincount(a[a >= 0].long(), minlength=shape.experts_per_rank) > 0).sum()))
+    # phase split: events around the three collectives (comm) and the compute between them
+    names = ["router", "allgather_logits", "select_pack", "alltoall_dispatch", "expert", "alltoall_return",
+             "combine"]
+    reps = min(20, args.steps)
+    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(reps)]
+    dist.barrier()
+    for i in range(reps):
+        EP.ep_layer(shape, ops[i % n], hid[i % n], mark=lambda j, _i=i: marks[_i][j].record())
+    torch.cuda.synchronize()
+    phase = [statistics.mean(marks[i][j].elapsed_time(marks[i][j + 1]) for i in range(reps)) for j in range(7)]
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -594,17 +720,14 @@ def run_ep(args, c, rank, world, local_rank):
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    crit = torch.tensor([float(statistics.mean(used_local))], dtype=torch.float64, device="cuda")  # same dtype on every rank
-    tot = crit.clone()
-    dist.all_reduce(crit, op=dist.ReduceOp.MAX)
-    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-
+    ms = _max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    stats = _ep_stats(used_local, world, c, ms, phase, names)
+    pm = stats["phase_ms_max_over_ranks"]
+    comm = pm["allgather_logits"] + pm["alltoall_dispatch"] + pm["alltoall_return"]
+    stats["comm_share"] = comm / sum(pm.values())
     # e2e: host-resident inputs/outputs per step
     h_host = [h.cpu().pin_memory() for h in hid]
-    o_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+    o_host = torch.empty((Tl, d), dtype=torch.bfloat16).pin_memory()
     dist.barrier()
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -616,30 +739,23 @@ def run_ep(args, c, rank, world, local_rank):
         o_host.copy_(out, non_blocking=True)
     c1.record()
     torch.cuda.synchronize()
-    me = torch.tensor([c0.elapsed_time(c1) / args.steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(me, op=dist.ReduceOp.MAX)
-    ms_e2e = float(me.item())
-    Tg = T * world
-    peak, peak_src = measured_peaks()
-    crit_bytes = float(crit.item()) * SWIGLU_BYTES(c)
-    return {
-        "metric": METRIC, "value": Tg / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic: random-init Mixtral-shaped bf16 weights, N(0,1) hidden",
-        "config": {"workload": c["workload"] + f"-ep{world}", "d_model": d, "d_ff": ff, "experts": N,
-                   "top_k": k, "global_batch": Tg, "tokens_per_gpu": T, "policy": f"{c['mode']} drop {c['drop']}",
-                   "parallelism": f"ep{world}", "weight_copies": n,
-                   "mean_used_experts_total": float(tot.item()), "critical_path_used_experts": float(crit.item())},
-        "roofline": {"bound": "hbm", "kernel": "ffn_kernel per rank (critical path)",
-                     "achieved": crit_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": crit_bytes / (ms * 1e-3) / 1e9 / peak, "peak_source": peak_src,
-                     "note": "critical-path bytes / whole step time (includes NCCL)", "traffic": None},
-        "e2e": {"value": Tg / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
-                "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
-        "gpu_launches": 6 * args.steps,
-        "clocks": clocks.summary(),
-    }
+    ms_e2e = _max_over_ranks(c0.elapsed_time(c1) / args.steps)
+    return _ep_result(args, c, world, Tl, ms, ms_e2e, stats, "NCCL all_gather + all_to_all_single (torch.distributed)",
+                      "ffn_kernel per rank (critical path)", 6, clocks)
+
+
+def self_launch(args) -> int:
+    """--gpus N without torchrun: re-run this script under torch.distributed.run
+    with N local ranks (rendezvous on 127.0.0.1)."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("launching", " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 def main():
@@ -654,6 +770,9 @@ def main():
                     help="N>1 on ONE GPU (gloo + CUDA IPC): functional check only, not a measurement")
     ap.add_argument("--ep-transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1: expert-parallel exchange over NVLink peer memory or NCCL collectives")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N>1: strong = the config's batch is the global batch (T/N rows per rank); "
+                         "weak = T rows per rank")
     ap.add_argument("--tokens", type=int, default=None, help="override the config's batch (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -662,11 +781,19 @@ def main():
     if args.tokens:
         c["T"] = args.tokens
         c["workload"] += f"-T{args.tokens}"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         return run_reference(args, c)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1 and (c["N"] % world or (args.scaling == "strong" and c["T"] % world)):
+        raise SystemExit(f"{c['N']} experts / batch {c['T']} do not shard over {world} GPUs")
+    if world > 1 and "layers" in c:
+        raise SystemExit("the 32-layer stack (c3) runs on one GPU")
 
     import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.share_gpu:  # functional check of the N>1 path with every rank on GPU 0 (timings meaningless)
@@ -679,15 +806,17 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        result = None
+        peers = None
         if args.ep_transport == "p2p":
-            try:
-                result = run_ep_p2p(args, c, rank, world, local_rank)
-            except Exception as e:  # symmetric memory unavailable -> NCCL collectives
+            from paper_2411_08982_b200 import ep_p2p as P2P
+            Tl = c["T"] // world if args.scaling == "strong" else c["T"]
+            try:  # collective: every rank gets the same outcome, so every rank takes the same branch
+                peers = P2P.ipc_peers(dist.group.WORLD, Tl, c["N"], c["d"])
+            except Exception as e:
                 log(f"peer-memory EP unavailable ({type(e).__name__}: {e}); using NCCL collectives")
-                torch.cuda.synchronize()
-                dist.barrier()
-        if result is None:
+        if peers is not None:
+            result = run_ep_p2p(args, c, rank, world, local_rank, peers)
+        else:
             result = run_ep(args, c, rank, world, local_rank)
     elif "layers" in c:
         result = run_stack(args, c)
@@ -696,6 +825,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(c)
+            result["cpu_baseline_f64_tanh2"] = cpu_baseline_tanh2(c)
         print(json.dumps(result), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -219,6 +219,13 @@ int lynx_moe_layer_profiled(const lynx_layer_t *layer, const uint16_t *hidden, i
                             void *workspace, size_t workspace_bytes, lynx_stream_t stream,
                             void *const *events, int n_events);
 
+/* Which K3 kernel lynx_moe_layer launches for this layer, batch and policy:
+ * 0 = ffn_kernel (one CTA per SM, tcgen05 cta_group::1), 1 = ffn_pair_kernel
+ * (CTA pairs, cta_group::2, for wide expert segments); negative = lynx_status.
+ * *stage_rows (may be NULL) receives the launch's activation tile width. */
+int lynx_moe_ffn_kernel(const lynx_layer_t *layer, int T, int decode, const lynx_policy_t *policy,
+                        int32_t *stage_rows);
+
 /* Pack HF-layout gate/up projections w1, w3 [N, ff, d] into the
  * interleaved w13 layout the SwiGLU kernel streams. */
 int lynx_pack_w13(const uint16_t *w1, const uint16_t *w3, int N, int ff, int d, uint16_t *w13,

@@ -85,6 +85,83 @@ def _pairwise(a, lo, n):
 
 
 # --------------------------------------------------------------------------
+# numpy's float64 exp (the reference's np.exp, router.py:153)
+# --------------------------------------------------------------------------
+
+# numpy 2.x on x86-64 AVX512_SKX hosts (this build container, which made
+# tests/golden/) computes float64 exp with the Intel SVML routine bundled in
+# numpy (__svml_exp8_ha, numpy/_core/src/umath/svml).  It is NOT correctly
+# rounded, so the device restates it step for step (csrc/npexp.cuh).  The
+# constants below are that routine's (read from numpy 2.3.5's
+# _multiarray_umath data table __svml_dexp_ha_data_internal_avx512):
+# 2^(j/16) = _EXP_HI[j] + _EXP_LO[j], ln2 = _LN2_HI + _LN2_LO, and the
+# degree-5 polynomial _EXP_C for (e^r - 1) / r.
+_EXP_HI = [float.fromhex(h) for h in (
+    "0x1.0000000000000p+0", "0x1.0b5586cf9890fp+0", "0x1.172b83c7d517bp+0", "0x1.2387a6e756238p+0",
+    "0x1.306fe0a31b715p+0", "0x1.3dea64c123422p+0", "0x1.4bfdad5362a27p+0", "0x1.5ab07dd485429p+0",
+    "0x1.6a09e667f3bcdp+0", "0x1.7a11473eb0187p+0", "0x1.8ace5422aa0dbp+0", "0x1.9c49182a3f090p+0",
+    "0x1.ae89f995ad3adp+0", "0x1.c199bdd85529cp+0", "0x1.d5818dcfba487p+0", "0x1.ea4afa2a490dap+0")]
+_EXP_LO = [float.fromhex(h) for h in (
+    "0x0p+0", "0x1.79aa65d837b6dp-54", "-0x1.01b15eaa59348p-55", "0x1.68efde3a8a894p-54",
+    "0x1.34d754db0abb6p-55", "0x1.59f48a72a4c6dp-55", "0x1.690cebb7aafb0p-56", "0x1.063e1e21c5409p-54",
+    "-0x1.3b3efbf5e2228p-54", "-0x1.b32dcb94da51dp-56", "0x1.db72fc1f0eab4p-55", "0x1.1affc2b91ce27p-56",
+    "0x1.c1a7792cb3387p-55", "0x1.36eae30af0cb3p-56", "0x1.4a385a63d07a7p-56", "-0x1.ff7128fd391f0p-55")]
+_LOG2E = float.fromhex("0x1.71547652b82fep+0")
+_SHIFT = float.fromhex("0x1.8000000003ff0p+48")
+_LN2_HI = float.fromhex("0x1.62e42fefa39efp-1")
+_LN2_LO = float.fromhex("0x1.abc9e3b39803fp-56")
+_EXP_C = [float.fromhex(h) for h in (  # c0 .. c5
+    "0x1.fffffffffff70p-1", "0x1.000000000d008p-1", "0x1.5555553939732p-3",
+    "0x1.55557242d68fep-5", "0x1.1101cbbc265c0p-7", "0x1.7411836940c04p-10")]
+_EXP_RARE = float.fromhex("0x1.61da04cbafe44p+9")
+
+
+def _fma(a: float, b: float, c: float, toward_zero: bool = False) -> float:
+    """a*b + c with one rounding (exact rational arithmetic), nearest-even or toward zero."""
+    from fractions import Fraction
+    exact = Fraction(a) * Fraction(b) + Fraction(c)
+    f = float(exact)  # correctly rounded to nearest
+    if toward_zero and Fraction(f) != exact and abs(Fraction(f)) > abs(exact):
+        import math
+        f = math.nextafter(f, 0.0)
+    return f
+
+
+def svml_exp_ha(x: float) -> float:
+    """np.exp(x) for float64 on AVX512_SKX hosts, restated step for step
+    (the same steps as csrc/npexp.cuh np_exp).  |x| >= 707.7 and NaN take
+    SVML's scalar fallback, which this restatement does not cover."""
+    import math
+    x = float(x)
+    if not abs(x) < _EXP_RARE:
+        raise OracleError("svml_exp_ha: argument outside the vector path")
+    t = _fma(x, _LOG2E, _SHIFT, toward_zero=True)
+    n = t - _SHIFT
+    j = int(np.array(t).view(np.uint64)) & 15
+    r = _fma(-n, _LN2_HI, x)
+    r = _fma(-_LN2_LO, n, r)
+    r2 = r * r
+    c0, c1, c2, c3, c4, c5 = _EXP_C
+    p = _fma(c5, r, c4)
+    q = _fma(c3, r, c2)
+    s = _fma(c1, r, c0)
+    p = _fma(r2, p, q)
+    p = _fma(r2, p, s)
+    p = _fma(p, r, _EXP_LO[j])
+    p = _fma(_EXP_HI[j], p, _EXP_HI[j])
+    return math.ldexp(p, math.floor(n))
+
+
+def numpy_uses_svml_exp() -> bool:
+    """True when this numpy dispatches float64 exp to SVML (AVX512_SKX)."""
+    try:
+        from numpy._core._multiarray_umath import __cpu_features__ as f
+    except ImportError:  # pragma: no cover - numpy < 2
+        from numpy.core._multiarray_umath import __cpu_features__ as f
+    return bool(f.get("AVX512_SKX"))
+
+
+# --------------------------------------------------------------------------
 # routing (router.py)
 # --------------------------------------------------------------------------
 
@@ -362,7 +439,7 @@ def silu(x):
 
 
 def forward_swiglu(hidden, w1, w3, w2, assigned, weights, dtype=np.float32,
-                   round_h_bf16: bool = False, shared=()):
+                   round_h_bf16: bool = False, shared=(), residual: bool = True):
     """forward_layer (simulator.py:86-113) with a SwiGLU expert.
 
     hidden [T, d]; w1, w3 [E, ff, d]; w2 [E, d, ff] (HF Mixtral / K-major
@@ -373,12 +450,15 @@ def forward_swiglu(hidden, w1, w3, w2, assigned, weights, dtype=np.float32,
     ``shared`` lists always-on experts (indices into w1/w3/w2) applied to
     every token with weight 1 after the routed experts, in the given order
     -- the builder's DeepSeek-MoE extension; the reference has none.
+    ``residual=False`` returns the expert sum alone (what
+    lynx_moe_forward_partial computes); w1/w3/w2 may be dicts holding only
+    the experts the mask uses.
     """
     x = np.asarray(hidden, dtype=dtype)
     if x.shape[0] != assigned.shape[0]:
         raise OracleError(
             f"mask covers {assigned.shape[0]} tokens but hidden has {x.shape[0]}")
-    out = x.copy()
+    out = x.copy() if residual else np.zeros_like(x)
     disp = dispatch(assigned, weights)
 
     def expert(e, xr):

@@ -22,7 +22,7 @@ LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "liblynx_b200.so")
 
 SOURCES = ["select.cu", "dispatch.cu", "ffn.cu", "attention.cu", "ep_p2p.cu", "capi.cu"]
-HEADERS = ["ptx.cuh", "lynx_internal.cuh", "p2p.cuh"]
+HEADERS = ["ptx.cuh", "lynx_internal.cuh", "p2p.cuh", "npexp.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-diag-suppress", "550"]

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get(
 
 # include/lynx_b200.h constants
 LYNX_OK = 0
-ABI_VERSION = 4
+ABI_VERSION = 5
 STATUS = {
     -1: "invalid shape", -2: "k out of range", -3: "min_experts must be >= top_k",
     -4: "retained set empty or out of range", -5: "token count mismatch", -6: "CUDA error",
@@ -100,6 +100,7 @@ _SIGS = {
     "lynx_moe_layer": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_layer_logits": (_i, [_p, _p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "lynx_moe_layer_profiled": (_i, [_p, _p, _i, _i, _p, _p, _p, _p, ctypes.c_size_t, _p, _p, _i]),
+    "lynx_moe_ffn_kernel": (_i, [_p, _i, _i, _p, _p]),
     "lynx_pack_w13": (_i, [_p, _p, _i, _i, _i, _p, _p]),
     "lynx_attention_workspace_bytes": (ctypes.c_size_t, [_i, _i]),
     "lynx_attention": (_i, [_p, _p, _i, _i, _i, _p, _p, _p, ctypes.c_size_t, _p]),

@@ -21,7 +21,7 @@ using namespace lynx;
 
 namespace {
 
-constexpr int kAbiVersion = 4;
+constexpr int kAbiVersion = 5;
 
 int sm_count_cached() {
   static int cached_dev = -1, cached = 0;
@@ -389,6 +389,13 @@ int check_peers(const lynx_ep_peers_t* P) {
   return LYNX_OK;
 }
 
+// Experts the policy is expected to keep: K3's kernel choice only (no effect on results).
+int kept_hint(const lynx_policy_t* policy, int decode, int N, int floor_keep) {
+  if (policy && decode && policy->mode == LYNX_POLICY_LATENCY) return std::max(floor_keep, N - policy->drop_count);
+  if (policy && decode && policy->mode == LYNX_POLICY_ACCURACY) return std::max(floor_keep, policy->freq_keep_budget);
+  return N;
+}
+
 int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int decode, const lynx_policy_t* policy,
                    uint16_t* out, const lynx_selection_t* sel, void* workspace, size_t workspace_bytes,
                    cudaStream_t stream, cudaEvent_t const* ev, const double* given_logits = nullptr) {
@@ -430,6 +437,7 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   a.flags = LYNX_PICK(flags, flags, int32_t);
 #undef LYNX_PICK
   a.plan = plan_out(ws, P, layer->num_shared);
+  a.routed_top = route_in_k0 ? 1 : 0;
   if (route_in_k0) {
     st = cuda_status(launch_router_route(hidden, layer->router_wt, T, layer->d_model, N, k, nullptr, a.full, a.ids,
                                          a.probs, stream));
@@ -438,13 +446,8 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   record(ev, 1, stream);
   st = cuda_status(launch_route_select(a, stream));
   if (st) return st;
-  // experts the policy is expected to keep (K3's kernel choice; no effect on results)
-  int kept = N;
-  if (policy && decode && policy->mode == LYNX_POLICY_LATENCY)
-    kept = std::max(floor_keep, N - policy->drop_count);
-  else if (policy && decode && policy->mode == LYNX_POLICY_ACCURACY)
-    kept = std::max(floor_keep, policy->freq_keep_budget);
-  st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr, nullptr, kept);
+  st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr, nullptr,
+                      kept_hint(policy, decode, N, floor_keep));
   record(ev, 5, stream);
   return st;
 }
@@ -647,6 +650,20 @@ int lynx_moe_layer_profiled(const lynx_layer_t* layer, const uint16_t* hidden, i
   if (!events || n_events != LYNX_PROFILE_EVENTS) return LYNX_ERR_SHAPE;
   return moe_layer_impl(layer, hidden, T, decode, policy, out, sel, workspace, workspace_bytes, stream,
                         reinterpret_cast<cudaEvent_t const*>(events));
+}
+
+int lynx_moe_ffn_kernel(const lynx_layer_t* layer, int T, int decode, const lynx_policy_t* policy,
+                        int32_t* stage_rows) {
+  int st = check_layer(layer, T);
+  if (st) return st;
+  int floor_keep = layer->top_k;
+  st = check_policy(policy, layer->top_k, decode, &floor_keep);
+  if (st) return st;
+  const Geometry g = geometry(layer, T);
+  const int N = layer->num_experts;
+  const int kept = std::min(kept_hint(policy, decode, N, floor_keep), N);
+  if (stage_rows) *stage_rows = g.bn;
+  return ffn_use_pair(g.bn, T * layer->top_k / kept) ? 1 : 0;
 }
 
 int lynx_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,

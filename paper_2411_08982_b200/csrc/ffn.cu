@@ -659,7 +659,7 @@ static cudaError_t launch_ffn_pair_t(const FfnParams& p, int sm_count, cudaStrea
 // rows: 468 -> 474 us; DeepSeek-MoE C4, ~37 rows: 76.5 -> 83.2 us).  The host
 // only knows the expected rows per used expert, so that picks the kernel.
 // LYNX_FFN_PAIR=0/1 forces either kernel (A/B switch); unset or "auto": by rows.
-static bool use_pair(int bn, int rows_hint) {
+bool ffn_use_pair(int bn, int rows_hint) {
   static int force = -2;
   if (force == -2) {
     const char* e = getenv("LYNX_FFN_PAIR");
@@ -688,7 +688,7 @@ static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s
 }
 
 cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, cudaStream_t s) {
-  const bool pair = use_pair(bn, rows_hint);
+  const bool pair = ffn_use_pair(bn, rows_hint);
   switch (bn) {
     case 32:
       return launch_ffn_t<32, 10>(p, sm_count, s);

@@ -33,9 +33,9 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 template <typename A>
 __device__ __forceinline__ void warm_params(const A& a) {
   constexpr int kLines = static_cast<int>((sizeof(A) + 31) / 32);
-  __shared__ int s_sink;  // a store keeps ptxas from dropping the loads
+  __shared__ int s_sink[kLines];  // one word per thread: a store keeps ptxas from dropping the load
   if (static_cast<int>(threadIdx.x) < kLines)
-    *static_cast<volatile int*>(&s_sink) = reinterpret_cast<const int*>(&a)[threadIdx.x * 8];
+    *static_cast<volatile int*>(&s_sink[threadIdx.x]) = reinterpret_cast<const int*>(&a)[threadIdx.x * 8];
 }
 
 template <typename... KArgs, typename... Args>
@@ -89,6 +89,7 @@ struct SelectArgs {
   lynx_policy_t pol;
   int floor_keep;  // resolved min_experts (>= k)
   int stage;       // stage per-token arrays in shared memory
+  int routed_top;  // given selection came from K0's routing: probs[:, :2] are the row's top two
   int32_t* ids;
   double* probs;
   double* full;
@@ -197,6 +198,8 @@ cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_poli
 cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s);
 // rows_hint: expected token rows per used expert (picks the CTA-pair kernel for wide segments)
 cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, cudaStream_t s);
+// K3 kernel choice: true -> ffn_pair_kernel (cta_group::2), false -> ffn_kernel
+bool ffn_use_pair(int bn, int rows_hint);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s);
 cudaError_t launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int N, int ff, int d, uint16_t* w13,
                             cudaStream_t s);

@@ -28,6 +28,7 @@
 #include <stdlib.h>
 
 #include "lynx_internal.cuh"
+#include "npexp.cuh"
 #include "p2p.cuh"
 #include "ptx.cuh"
 
@@ -542,9 +543,10 @@ __device__ __forceinline__ void batch_policy(const SelectArgs& a, const int32_t*
 // One thread per token with its whole probability row in registers: the N
 // exps are independent (they interleave), numpy's pairwise sum and the
 // stable top-k run on registers, and the same thread keeps its row from
-// routing through the remap.  Division by the row sum uses one IEEE
-// reciprocal per token (<= 1 ulp from numpy's e/s; decisions unchanged,
-// probabilities well within the 1e-12 contract).
+// routing through the remap.  Probabilities are np_exp(z - max) / sum --
+// numpy's exp bits, numpy's summation order and a true IEEE division -- so
+// full_probs equal the reference's bit for bit and float64 near-ties order
+// as they do there.
 template <int NT>
 __device__ __forceinline__ double reg_pairwise_sum(const double (&e)[NT], int n) {
   if (n < 8) {
@@ -646,10 +648,10 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
         }
       if (!finite) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
 #pragma unroll
-      for (int i = 0; i < NT; ++i) p[i] = i < N ? exp(p[i] - m) : 0.0;
-      const double inv = 1.0 / reg_pairwise_sum<NT>(p, N);
+      for (int i = 0; i < NT; ++i) p[i] = i < N ? np_exp(p[i] - m) : 0.0;
+      const double sum = reg_pairwise_sum<NT>(p, N);
 #pragma unroll
-      for (int i = 0; i < NT; ++i) p[i] *= inv;
+      for (int i = 0; i < NT; ++i) p[i] = p[i] / sum;  // e / s, as numpy divides (router.py:154)
       uint64_t taken = ~expert_mask_all(N);
 #pragma unroll 1
       for (int r = 0; r < k; ++r) {
@@ -740,11 +742,10 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
     }
     const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot_p, k);
     if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);
-    const double inv = 1.0 / total;
 #pragma unroll
     for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
       if (r >= k) break;
-      const double w = slot_p[r] * inv;
+      const double w = slot_p[r] / total;  // policy.py:208, 220
       ASG[t * k + r] = asg[r];
       WT[t * k + r] = w;
       a.assigned[t * k + r] = asg[r];
@@ -869,8 +870,7 @@ __device__ __forceinline__ int grp_best(const double (&v)[EPL], uint32_t cand, i
 // assignment and the slot probability (renormalised by the caller).
 template <int EPR>
 __device__ __forceinline__ void remap_row(const double* prow, bool live, int t, int k, int j, uint64_t keep, int nR,
-                                          const int* rlist, const int32_t* IDS, const double* PROBS, int32_t* ASG,
-                                          double* WT) {
+                                          const int* rlist, const int32_t* IDS, int32_t* ASG, double* WT) {
   double v[EPR];
 #pragma unroll
   for (int q = 0; q < EPR; ++q) {
@@ -893,7 +893,7 @@ __device__ __forceinline__ void remap_row(const double* prow, bool live, int t, 
       dmask |= 1u << r;
     if (live && j == 0) {
       ASG[t * k + r] = e;
-      WT[t * k + r] = PROBS[t * k + r];  // p[e] of the original (same bits as the row)
+      WT[t * k + r] = prow[e];  // full_probs[t, assigned] (policy.py:206-208)
     }
   }
   const int d = live ? __popc(dmask) : 0;
@@ -989,7 +989,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
       SEL_TS_LOCAL(8);
       if (bad) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
 #pragma unroll
-      for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? exp(v[q] - m) : 0.0;
+      for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m) : 0.0;
       SEL_TS_LOCAL(9);
       const double sum = grp_pairwise<EPL>(v, N, j, gbase);
       SEL_TS_LOCAL(10);
@@ -1025,12 +1025,15 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
         IDS[t * k + j] = a.ids[t * k + j];
         PROBS[t * k + j] = a.probs[t * k + j];
       }
-      // The confidence follows from the selection itself: top1 = the first
-      // pick's probability (the row max), margin = first - second pick
-      // (router.py:190-192).  The probability row is then never staged: the
-      // remap reads its retained entries straight from `full`.  A row routed
-      // from non-finite logits arrives with NaN probabilities.
-      if (a.pol.confidence_metric != LYNX_CONF_MARGIN || k >= 2) {
+      // A selection K0 routed itself (a.routed_top) has probs[:, 0] = the row
+      // max and probs[:, 1] = the second largest, bit for bit, so the
+      // confidence (router.py:125-138) follows from it: top1 = the first
+      // pick, margin = first - second pick.  The probability row is then never
+      // staged: the remap reads its retained entries straight from `full`.
+      // A row routed from non-finite logits arrives with NaN probabilities.
+      // Any other given selection (lynx_apply_policy: e.g. a deny-rank
+      // intervention, simulator.py:183-213) scores the full row below.
+      if (a.routed_top && (a.pol.confidence_metric != LYNX_CONF_MARGIN || k >= 2)) {
         if (live && j == 0) {
           const double p0 = a.probs[t * k], p1 = k > 1 ? a.probs[t * k + 1] : 0.0;
           if (isnan(p0)) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
@@ -1107,9 +1110,9 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
       // probabilities park in WT until the row's renormalisation.
       const double* prow = (kGiven ? a.full : P) + static_cast<size_t>(t) * N;
       if (EPL > 4 && nR <= 32)
-        remap_row<(EPL > 4 ? 4 : EPL)>(prow, live, t, k, j, keep, nR, s_rlist, IDS, PROBS, ASG, WT);
+        remap_row<(EPL > 4 ? 4 : EPL)>(prow, live, t, k, j, keep, nR, s_rlist, IDS, ASG, WT);
       else
-        remap_row<EPL>(prow, live, t, k, j, keep, nR, s_rlist, IDS, PROBS, ASG, WT);
+        remap_row<EPL>(prow, live, t, k, j, keep, nR, s_rlist, IDS, ASG, WT);
       SEL_TS_LOCAL(22);
     } else if (live && j == 0) {
 #pragma unroll 1
@@ -1323,10 +1326,15 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
   __shared__ double zs[LYNX_MAX_EXPERTS];
   cg::cluster_group cluster = cg::this_cluster();
   griddep_launch_dependents();
+  // DSMEM rule: the leader must have started before its shared memory is
+  // written.  Arrive now, wait just before the remote store, so the
+  // barrier's latency hides behind the dot products.
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const int t = blockIdx.y, c = static_cast<int>(cluster.block_rank());
   const int n0 = c * 8;
   griddep_wait();  // hidden may be produced by the previous kernel
   const double z = router_dots8(hidden, wt, t, d, N, n0);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
     double* zl = cluster.map_shared_rank(zs, 0);
     zl[n0 + threadIdx.x] = z;
@@ -1354,7 +1362,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
   m = fmax(m, __shfl_xor_sync(kFull, m, 4));
   bad = __any_sync(kFull, live && bad);
 #pragma unroll
-  for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? exp(v[q] - m) : 0.0;
+  for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m) : 0.0;
   const double sum = grp_pairwise<EPL>(v, N, j, gbase);
 #pragma unroll
   for (int q = 0; q < EPL; ++q) v[q] = v[q] / sum;  // e / s, as numpy divides

@@ -77,23 +77,37 @@ class EPOps:
         raise NotImplementedError
 
 
-def ep_layer(shape: EPShape, ops: EPOps, hidden_local, group=None):
-    """One expert-parallel MoE decode layer (steps 1-8 above)."""
+def ep_layer(shape: EPShape, ops: EPOps, hidden_local, group=None, mark=None):
+    """One expert-parallel MoE decode layer (steps 1-8 above).  ``mark(i)``
+    (optional, e.g. a CUDA event record) is called at the 8 phase
+    boundaries: before the router (0), the logits all-gather (1), select +
+    pack (2), the dispatch all-to-all (3), the expert FFN (4), the return
+    all-to-all (5), the combine (6) and after it (7)."""
     torch = _torch()
     import torch.distributed as dist
+    mark = mark or (lambda i: None)
     G, Tl, N, d = shape.world_size, shape.tokens_per_rank, shape.num_experts, shape.d_model
+    mark(0)
     logits_local = ops.router(hidden_local)
     logits_all = torch.empty((G * Tl, N), dtype=logits_local.dtype, device=logits_local.device)
+    mark(1)
     dist.all_gather_into_tensor(logits_all, logits_local.contiguous(), group=group)
+    mark(2)
     assigned, weights = ops.select(logits_all)
     send = ops.pack(hidden_local, assigned)
     recv = torch.empty_like(send)
+    mark(3)
     dist.all_to_all_single(recv, send, group=group)
+    mark(4)
     assigned_local, weights_local = ops.local_mask(assigned, weights)
     partial = ops.forward_partial(recv.view(G * Tl, d), assigned_local, weights_local)
     back = torch.empty_like(partial)
+    mark(5)
     dist.all_to_all_single(back, partial.contiguous(), group=group)
-    return ops.combine(hidden_local, back.view(G, Tl, d))
+    mark(6)
+    out = ops.combine(hidden_local, back.view(G, Tl, d))
+    mark(7)
+    return out
 
 
 class NativeEPOps(EPOps):

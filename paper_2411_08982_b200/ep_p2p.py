@@ -102,36 +102,81 @@ def symmetric_peers(group, Tl: int, N: int, d: int) -> PeerSet:
     return _make(G, rank, Tl, bufs, arrays, zeros((4,), torch.int32), zeros((1,), torch.int32))
 
 
+def _device_uuid(dev: int) -> str:
+    return str(_torch().cuda.get_device_properties(dev).uuid)
+
+
+def _local_ordinal(uuid: str) -> int:
+    """This process's ordinal of the GPU with `uuid`; -1 if it is not visible
+    (e.g. per-rank CUDA_VISIBLE_DEVICES isolation)."""
+    torch = _torch()
+    for i in range(torch.cuda.device_count()):
+        if _device_uuid(i) == uuid:
+            return i
+    return -1
+
+
 def ipc_peers(group, Tl: int, N: int, d: int) -> PeerSet:
     """This process's rank with buffers shared over CUDA IPC (cudaIpc*MemHandle
     through torch's storage sharing): works across GPUs of one node (the
     opened peer allocations are reached over NVLink) and for several
-    processes on one GPU, which is how it is tested here."""
+    processes on one GPU, which is how it is tested here.
+
+    Collective and all-or-nothing: every rank of `group` calls it, and it
+    either succeeds on every rank or raises ValidationError on every rank,
+    so callers can fall back (to NCCL) together without a hang.  Peer GPUs
+    are identified by UUID, not by the owner's device ordinal (ordinals are
+    per process: under CUDA_VISIBLE_DEVICES isolation every rank is device 0).
+    """
     torch = _torch()
     import torch.distributed as dist
     G, rank = dist.get_world_size(group), dist.get_rank(group)
     zeros = lambda shape, dt: torch.zeros(shape, dtype=dt, device="cuda")  # noqa: E731
-    bufs = _buffers(zeros, G, Tl, N, d)
-    torch.cuda.synchronize()
-    mine = {n: t.untyped_storage()._share_cuda_() for n, t in bufs.items()}
+    mine, bufs = {}, None
+    try:
+        bufs = _buffers(zeros, G, Tl, N, d)
+        torch.cuda.synchronize()
+        mine = {"uuid": _device_uuid(torch.cuda.current_device()),
+                "h": {n: t.untyped_storage()._share_cuda_() for n, t in bufs.items()}}
+    except Exception as e:  # still join the exchange below, so no rank is left waiting
+        mine = {"error": f"rank {rank}: {type(e).__name__}: {e}"}
     allh = [None] * G
     dist.all_gather_object(allh, mine, group=group)
-    # Opened IPC allocations are mapped for their owner's device only; our
-    # kernels run on this rank's device and store into them over NVLink.
-    here = torch.cuda.current_device()
-    for dev in sorted({allh[r][n][0] for r in range(G) if r != rank for n in bufs} - {here}):
-        nat.check(nat.lib().lynx_enable_peer_access(int(dev)), "lynx_enable_peer_access")
-    opened, arrays = [], {}
-    for n, t in bufs.items():
-        ptrs = []
-        for r in range(G):
-            if r == rank:
-                ptrs.append(t.data_ptr())
-                continue
-            st = torch.UntypedStorage._new_shared_cuda(*allh[r][n])
-            opened.append(st)
-            ptrs.append(st.data_ptr())
-        arrays[n] = _ptr_array(ptrs)
+    errors = [a["error"] for a in allh if "error" in a]
+    opened, arrays, err = [], {}, None
+    if not errors:
+        try:
+            here = torch.cuda.current_device()
+            local = []
+            for r in range(G):
+                dev = _local_ordinal(allh[r]["uuid"])
+                if dev < 0:
+                    raise ValidationError(f"rank {r}'s GPU {allh[r]['uuid']} is not visible to rank {rank} "
+                                          "(per-rank device isolation?): peer memory needs every GPU visible")
+                local.append(dev)
+            # Opened IPC allocations are mapped for their owner's device; our
+            # kernels run on this rank's device and store into them over NVLink.
+            for dev in sorted(set(local) - {here}):
+                nat.check(nat.lib().lynx_enable_peer_access(int(dev)), "lynx_enable_peer_access")
+            for n, t in bufs.items():
+                ptrs = []
+                for r in range(G):
+                    if r == rank:
+                        ptrs.append(t.data_ptr())
+                        continue
+                    h = allh[r]["h"][n]
+                    st = torch.UntypedStorage._new_shared_cuda(local[r], *h[1:])
+                    opened.append(st)
+                    ptrs.append(st.data_ptr())
+                arrays[n] = _ptr_array(ptrs)
+            torch.cuda.synchronize()
+        except Exception as e:
+            err = f"rank {rank}: {type(e).__name__}: {e}"
+    status = [None] * G
+    dist.all_gather_object(status, err, group=group)
+    errors += [e for e in status if e]
+    if errors:
+        raise ValidationError("CUDA-IPC peer buffers unavailable: " + "; ".join(errors))
     dist.barrier(group)
     ps = _make(G, rank, Tl, bufs, arrays, zeros((4,), torch.int32), zeros((1,), torch.int32))
     ps.keep = ps.keep + (opened,)

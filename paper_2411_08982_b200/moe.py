@@ -420,6 +420,16 @@ class LynxMoELayer:
         nat.check(st, "lynx_moe_layer_profiled")
         return out
 
+    def ffn_kernel(self) -> str:
+        """The K3 kernel this layer launches: "ffn_pair_kernel" (tcgen05
+        cta_group::2, wide expert segments) or "ffn_kernel" (lynx_moe_ffn_kernel)."""
+        rows = ctypes.c_int32()
+        r = self._lib.lynx_moe_ffn_kernel(self._layer_ref, self.T, 1 if self.phase is Phase.DECODE else 0,
+                                          self._pol_ref, ctypes.byref(rows))
+        if r < 0:
+            nat.check(r, "lynx_moe_ffn_kernel")
+        return "ffn_pair_kernel" if r == 1 else "ffn_kernel"
+
     def used_experts(self) -> int:
         """Experts streamed by the last call: routed experts with >= 1 assigned
     slot plus the shared experts (host sync; reporting only)."""

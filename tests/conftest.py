@@ -48,6 +48,11 @@ def selection_golden():
 
 
 @pytest.fixture(scope="session")
+def neartie64_golden():
+    return load_cases("selection_neartie64.npz")
+
+
+@pytest.fixture(scope="session")
 def remap_golden():
     return load_cases("remap.npz")
 

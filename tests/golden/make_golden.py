@@ -20,6 +20,8 @@ Cases:
                     C4 128x64 k6, C5 256x8 k2) and random small shapes,
                     both policies, both phases, ties / near-ties /
                     clustered logits.
+  selection_neartie64.npz -- float64-ulp near-ties (top-2, k/k+1 boundary,
+                    random) at the C2/C5/C4 routing shapes, both policies.
   remap.npz      -- remap_tokens on arbitrary retained sets incl. collapse.
   forward.npz    -- forward_layer (tanh2 reference expert) outputs, plus
                     the per-expert dispatch order and merged weights
@@ -230,6 +232,54 @@ def selection_cases():
     return cases
 
 
+def neartie64_cases():
+    """Float64-ulp near-ties at the BASELINE routing shapes (own RNG, so the
+    other fixtures are unchanged).  Logits one or a few float64 ulps apart --
+    at the row max, at the k / k+1 boundary and in random places -- make the
+    reference's order depend on the last bit of e / e.sum() (router.py:152-154,
+    181), so a device softmax that differs from numpy by one ulp anywhere
+    (exp, the row sum, the division) flips ids here."""
+    rng = np.random.default_rng(64064)
+    cases = []
+
+    def nudge(x, steps, up):
+        for _ in range(steps):
+            x = np.nextafter(x, np.inf if up else -np.inf)
+        return x
+
+    def make(T, N, k, where):
+        z = rng.normal(0.0, 2.0, size=(T, N))
+        for t in range(T):
+            order = np.argsort(-z[t], kind="stable")
+            if where == "top":
+                a, b = order[0], order[1]
+            elif where == "boundary":
+                a, b = order[k - 1], order[min(k, N - 1)]
+            else:
+                a, b = rng.choice(N, size=2, replace=False)
+            z[t, b] = nudge(z[t, a], int(rng.integers(0, 3)), bool(rng.random() < 0.5))
+            if rng.random() < 0.3 and N > 2:  # a third expert in the same ulp cluster
+                c = [e for e in range(N) if e not in (a, b)][int(rng.integers(0, N - 2))]
+                z[t, c] = nudge(z[t, a], int(rng.integers(1, 3)), bool(rng.random() < 0.5))
+        return z
+
+    shapes = [(32, 8, 2), (256, 8, 2), (64, 8, 2), (16, 16, 4), (128, 64, 6)]
+    for (T, N, k) in shapes:
+        for where in ("top", "boundary", "random"):
+            z = make(T, N, k, where)
+            tag = f"neartie64-{T}x{N}-{where}"
+            cfgs = [PolicyConfig(mode="latency", drop_count=N // 2),
+                    PolicyConfig(mode="accuracy", confidence_threshold=0.3, freq_keep_budget=max(1, N // 4),
+                                 confidence_metric="margin"),
+                    PolicyConfig(mode="accuracy", confidence_threshold=0.5, freq_keep_budget=max(1, N // 4))]
+            for cfg in cfgs:
+                out = run_selection(z, k, cfg, Phase.DECODE)
+                cases.append((dict(k=k, cfg=pack_cfg(cfg), phase=Phase.DECODE.value, tag=tag), out))
+            out = run_selection(z, k, None, Phase.DECODE)
+            cases.append((dict(k=k, cfg=None, phase=Phase.DECODE.value, tag=tag + "-identity"), out))
+    return cases
+
+
 def remap_cases():
     rng = np.random.default_rng(77)
     cases = []
@@ -312,11 +362,15 @@ def main():
     save("selection.npz", sel, meta=dict(
         source="moetrim 0.1.0 (/root/reference/pkg/src), numpy " + np.__version__,
         cases=[m for m, _ in sel]))
+    nt = neartie64_cases()
+    save("selection_neartie64.npz", nt, meta=dict(
+        source="moetrim 0.1.0 (/root/reference/pkg/src), numpy " + np.__version__,
+        cases=[m for m, _ in nt]))
     rem = remap_cases()
     save("remap.npz", rem, meta=dict(n=len(rem)))
     fwd = forward_cases()
     save("forward.npz", fwd, meta=dict(n=len(fwd)))
-    print(f"selection {len(sel)} remap {len(rem)} forward {len(fwd)}")
+    print(f"selection {len(sel)} neartie64 {len(nt)} remap {len(rem)} forward {len(fwd)}")
 
 
 if __name__ == "__main__":

@@ -226,24 +226,33 @@ def test_p2p_ep_two_processes_one_gpu():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("config", ["c2", "c5"])
-def test_bench_multi_rank_path_runs(config):
-    """bench.py's N>1 path as the driver launches it (torchrun, one rank per
-    GPU), here with all four ranks sharing GPU 0 (--share-gpu, gloo): the
-    peer-memory EP step, the max-over-ranks timing and the e2e leg must run
-    to one JSON line.  Per-rank statistics differ between ranks, so every
-    collective must use one dtype on all ranks."""
+@pytest.mark.parametrize("config,transport,batch", [("c2", "p2p", 32), ("c5", "p2p", 256), ("c5", "nccl", 256)])
+def test_bench_multi_rank_path_runs(config, transport, batch):
+    """bench.py --gpus 4 WITHOUT torchrun: it re-launches itself with four
+    local ranks (here all on GPU 0: --share-gpu, gloo), runs the EP step at
+    the config's fixed global batch (C5: decode batch 256 = 64 rows per rank)
+    and prints one JSON line with the per-rank / critical-path / aggregate
+    bytes.  Per-rank statistics differ between ranks, so every collective
+    must use one dtype on all ranks."""
     import json
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "4",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
-           "--gpus", "4", "--share-gpu", "--config", config, "--steps", "4", "--warmup", "3"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--share-gpu", "--config", config,
+           "--ep-transport", transport, "--steps", "4", "--warmup", "3"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root, env=env)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 4 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["n_gpus"] == 4 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["parallelism"] == "ep4"
+    assert d["config"]["global_batch"] == batch and d["config"]["tokens_per_gpu"] == batch // 4
+    run = d["run"]
+    assert len(run["used_experts_per_rank"]) == 4
+    assert run["critical_path_bytes"] == max(run["expert_bytes_per_rank"])
+    assert abs(run["aggregate_bytes"] - sum(run["expert_bytes_per_rank"])) < 1
+    assert ("nccl" in run["transport"].lower()) == (transport == "nccl")
+    if transport == "nccl":
+        assert 0 <= run["comm_share"] <= 1

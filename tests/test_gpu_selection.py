@@ -1,8 +1,12 @@
 """GPU parity: routing + retention policies vs the reference's golden vectors.
 
 Bit-exact for every decision (ids, retained set, remap, important tokens,
-clipped flag); float64 probabilities / weights / confidences within 1e-12
-(CUDA exp vs numpy's SIMD exp differ by <= 1 ulp).
+clipped flag) and -- since the device softmax restates numpy's own float64
+exp (csrc/npexp.cuh), pairwise row sum and division -- for the float64
+probabilities, confidences and weights too, on the fixtures made on the
+generator machine (tests/golden/make_golden.py).  Comparisons against the
+oracle run on the GPU box's own numpy keep 1e-12 for floats (its numpy may
+take another exp path).
 """
 
 from __future__ import annotations
@@ -104,6 +108,110 @@ def test_golden_through_c_abi_single_launch(selection_golden):
         assert np.array_equal(_np(out["imp"]), c["important"]), tag
         assert bool(_np(out["flags"])[0] & nat.FLAG_CLIPPED) == bool(c["clipped"]), tag
         assert np.array_equal(_np(out["counts"]), c["counts"]), tag
+
+
+def _c_abi_select(c):
+    meta = c["meta"]
+    z = torch.from_numpy(c["logits"]).cuda()
+    T, N = z.shape
+    k = meta["k"]
+    out = {n: torch.zeros(s, dtype=dt, device="cuda") for n, s, dt in [
+        ("ids", (T, k), torch.int32), ("probs", (T, k), torch.float64), ("full", (T, N), torch.float64),
+        ("conf", (T,), torch.float64), ("counts", (N,), torch.float64), ("ret", (N,), torch.uint8),
+        ("asg", (T, k), torch.int32), ("w", (T, k), torch.float64), ("imp", (T,), torch.uint8),
+        ("flags", (1,), torch.int32)]}
+    sel = nat.LynxSelection(expert_ids=out["ids"].data_ptr(), probs=out["probs"].data_ptr(),
+                            full_probs=out["full"].data_ptr(), conf=out["conf"].data_ptr(),
+                            counts=out["counts"].data_ptr(), retained=out["ret"].data_ptr(),
+                            assigned=out["asg"].data_ptr(), weights=out["w"].data_ptr(),
+                            important=out["imp"].data_ptr(), flags=out["flags"].data_ptr())
+    cfg = _policy(meta)
+    pol = None if cfg is None else ctypes.cast(ctypes.pointer(cfg.to_native()), ctypes.c_void_p)
+    st = nat.lib().lynx_route_select(z.data_ptr(), T, N, k, 1 if meta["phase"] == "decode" else 0, pol,
+                                     ctypes.cast(ctypes.pointer(sel), ctypes.c_void_p),
+                                     torch.cuda.current_stream().cuda_stream)
+    assert st == 0, st
+    torch.cuda.synchronize()
+    return {n: _np(t) for n, t in out.items()}
+
+
+def test_neartie64_golden_bit_exact(neartie64_golden):
+    """Float64-ulp near-ties (top-2, k/k+1 boundary, random) at the C2/C5/C4
+    routing shapes: the reference's order depends on the last bit of
+    e / e.sum() (router.py:152-154, 181).  Every output -- ids, probabilities,
+    the full softmax, confidences, the policy's decisions and the remap
+    weights -- equals the reference's bit for bit, through the C ABI (one
+    launch) and through the mirror API."""
+    assert len(neartie64_golden) == 60
+    for i, c in enumerate(neartie64_golden):
+        meta = c["meta"]
+        tag = (i, meta["tag"])
+        o = _c_abi_select(c)
+        assert np.array_equal(o["ids"], c["expert_ids"]), tag
+        assert np.array_equal(o["probs"], c["probs"]), tag
+        assert np.array_equal(o["full"], c["full_probs"]), tag
+        assert np.array_equal(o["ret"], c["retained"]), tag
+        assert np.array_equal(o["asg"], c["assigned"]), tag
+        assert np.array_equal(o["w"], c["weights"]), tag
+        assert np.array_equal(o["imp"], c["important"]), tag
+        assert bool(o["flags"][0] & nat.FLAG_CLIPPED) == bool(c["clipped"]), tag
+        assert np.array_equal(o["counts"], c["counts"]), tag
+        cfg = _policy(meta)
+        metric = cfg.confidence_metric if cfg is not None else "top1"
+        if cfg is not None:
+            assert np.array_equal(o["conf"], c["conf"]), tag
+        sel = L.route_batch(L.RoutingLogits(0, L.Phase.DECODE, c["logits"]), meta["k"])
+        assert np.array_equal(_np(sel.expert_ids), c["expert_ids"]), tag
+        assert np.array_equal(_np(sel.full_probs), c["full_probs"]), tag
+        assert np.array_equal(_np(sel.confidence(metric)), c["conf"]), tag
+        mask = L.full_retain_mask(sel, 0, L.Phase.DECODE) if cfg is None else L.apply_policy(sel, L.Phase.DECODE, cfg)
+        assert np.array_equal(_np(mask.remap_assigned), c["assigned"]), tag
+        assert np.array_equal(_np(mask.remap_weights), c["weights"]), tag
+
+
+def test_golden_probabilities_bit_exact(selection_golden):
+    """The 333 reference selection cases: the float64 softmax, top-k
+    probabilities and remap weights carry the reference's exact bits."""
+    for i, c in enumerate(selection_golden):
+        tag = (i, c["meta"]["tag"])
+        o = _c_abi_select(c)
+        assert np.array_equal(o["probs"], c["probs"]), tag
+        if "full_probs" in c:
+            assert np.array_equal(o["full"], c["full_probs"]), tag
+        assert np.array_equal(o["w"], c["weights"]), tag
+
+
+@pytest.mark.parametrize("T,N,k", [(2000, 64, 6), (2000, 8, 2), (40, 64, 6)])
+def test_deny_rank_selection_scores_confidence_on_full_row(T, N, k):
+    """apply_policy on a selection whose rank 0 is NOT the row's arg-max (the
+    reference's deny_expert_rank intervention, simulator.py:183-213): the
+    confidence is the full row's max / top-2 margin (router.py:125-138), so
+    the accuracy policy's important tokens follow the oracle.  T=2000 or
+    N=64 run K1's group path on a given selection."""
+    rng = np.random.default_rng(T + N)
+    z = rng.normal(0, 2.0, size=(T, N))
+    ids, probs, full = O.route(z, k)
+    den = ids.copy()  # deny rank 0: best unselected expert, slots re-sorted by (p desc, id asc)
+    for t in range(T):
+        chosen = set(int(e) for e in den[t])
+        order = sorted(range(N), key=lambda e: (-full[t, e], e))
+        den[t, 0] = next(e for e in order if e not in chosen)
+        p = full[t, den[t]]
+        den[t] = den[t][np.lexsort((den[t], -p))]
+    dprobs = np.take_along_axis(full, den, axis=1)
+    sel = L.ExpertSelection(expert_ids=den, probs=dprobs, full_probs=full)
+    for metric in ("top1", "margin"):
+        assert close(_np(sel.confidence(metric)), O.confidence(full, metric))
+        pol = O.Policy(mode="accuracy", confidence_threshold=0.3 if metric == "top1" else 0.1, sample_threshold=8,
+                       freq_keep_budget=max(1, N // 4), confidence_metric=metric)
+        m = O.apply(den, dprobs, full, pol)
+        cfg = L.PolicyConfig(mode="accuracy", confidence_threshold=pol.confidence_threshold, sample_threshold=8,
+                             freq_keep_budget=pol.freq_keep_budget, confidence_metric=metric)
+        mask = L.apply_policy(sel, L.Phase.DECODE, cfg)
+        assert np.array_equal(_np(mask.important_tokens), m.important), metric
+        assert np.array_equal(_np(mask.retained), m.retained), metric
+        assert np.array_equal(_np(mask.remap_assigned), m.assigned), metric
+        assert close(_np(mask.remap_weights), m.weights), metric
 
 
 def test_remap_golden(remap_golden):

@@ -85,6 +85,36 @@ class TestSelectionGolden:
         assert np.array_equal(mask.weights, c["weights"])
 
 
+class TestNumpyExp:
+    """The SVML exp restatement (oracle.svml_exp_ha, the same steps as
+    csrc/npexp.cuh) against this host's np.exp, bit for bit."""
+
+    def test_matches_numpy_bitwise(self):
+        if not O.numpy_uses_svml_exp():
+            pytest.skip("this numpy does not dispatch float64 exp to SVML (no AVX512_SKX)")
+        rng = np.random.default_rng(7)
+        xs = np.concatenate([-np.abs(rng.normal(0, 4, 4000)), -rng.uniform(0, 1e-3, 500),
+                             -rng.uniform(0, 700, 500), rng.normal(0, 3, 500),
+                             [0.0, -0.0, -1e-300, -5e-324, -1e-17, -np.log(2) / 16, -707.0, 700.0]])
+        got = np.array([O.svml_exp_ha(x) for x in xs])
+        assert np.array_equal(got, np.exp(xs))
+
+    def test_neartie64_fixtures_bit_exact(self, neartie64_golden):
+        """Float64-ulp near-ties: the oracle reproduces the reference's bits."""
+        for i, c in enumerate(neartie64_golden):
+            ids, probs, full, conf, mask = oracle_select(c)
+            tag = (i, c["meta"]["tag"])
+            if not np.array_equal(full, c["full_probs"]):
+                pytest.skip("different numpy exp build than the fixture machine")
+            assert np.array_equal(ids, c["expert_ids"]), tag
+            assert np.array_equal(conf, c["conf"]), tag
+            assert np.array_equal(mask.assigned, c["assigned"]), tag
+            assert np.array_equal(mask.weights, c["weights"]), tag
+            keep = np.zeros(full.shape[1], dtype=np.uint8)
+            keep[mask.retained] = 1
+            assert np.array_equal(keep, c["retained"]), tag
+
+
 class TestRemapGolden:
     def test_all_cases(self, remap_golden):
         for i, c in enumerate(remap_golden):
