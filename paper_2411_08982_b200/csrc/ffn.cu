@@ -415,13 +415,29 @@ __device__ __forceinline__ bool decode_unit_pair(const FfnParams& p, int nseg, i
   return true;
 }
 
-template <int BN, int STAGES>
+// Ring bytes of the CTA-pair kernel: STAGES stages of the widest stage
+// (MT = 1), or the shared-memory budget carved at run time (MT = 2: 4 stages
+// at 256 token rows, 5 at 128, 6 at 64).
+constexpr int pair_ring_bytes(int BN, int STAGES, int MT) {
+  return MT == 1 ? STAGES * (kTileA + BN * 64) : 216 * 1024;
+}
+
+// MT weight tiles per CTA per stage: a pair unit covers 256 * MT weight rows
+// (MMA j takes rows 256 j + 128 r .. of the unit on CTA r), all against the
+// same activation tile.  Each SM then pulls 1/MT of the activation bytes per
+// weight byte through L2: at large batches the L2 -> SM traffic (weights +
+// activations) is what caps the weight stream, not HBM.  The MT accumulators
+// of a unit take MT * N TMEM columns; they are double-buffered when two
+// units' worth fit (N <= 256 / MT), else the epilogue drains one unit while
+// the MMA waits for it.
+template <int BN, int STAGES, int MT>
 __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_constant__ FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int kRing = STAGES * (kTileA + BN * 64);
-  constexpr uint32_t kTmemCols = 2 * BN;
-  uint8_t* ring = smem;  // stage s: [weights 16 KB | this CTA's half of the token rows]
+  constexpr int kRing = pair_ring_bytes(BN, STAGES, MT);
+  constexpr uint32_t kTmemCols = 512;
+  static_assert(MT * BN <= 512, "a unit's accumulators must fit TMEM");
+  uint8_t* ring = smem;  // stage s: [MT weight tiles x 16 KB | this CTA's half of the token rows]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRing);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
@@ -464,11 +480,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
   griddep_wait();
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
-  const int tp1 = (p.tiles1 + 1) >> 1, tp2 = (p.tiles2 + 1) >> 1;
+  const int tp1 = (p.tiles1 + 2 * MT - 1) / (2 * MT), tp2 = (p.tiles2 + 2 * MT - 1) / (2 * MT);
   const int total = nseg * (tp1 + tp2 * p.split2);
   const int width = p.max_rows ? min(BN, max(32, (*p.max_rows + 31) & ~31)) : BN;
-  const int stage_bytes = kTileA + (width >> 1) * 128;
+  const int stage_bytes = MT * kTileA + (width >> 1) * 128;
   const int nstages = min(kMaxStages, kRing / stage_bytes);
+  const int nacc = 2 * MT * width <= static_cast<int>(kTmemCols) ? 2 : 1;  // accumulator buffers
+  const int acc_cols = MT * width;  // column stride of the two buffers (2 * MT * width <= 512 when nacc == 2)
   const uint32_t peer_ufull = mapa_shared(ufull, 1), peer_uring = mapa_shared(uring, 1);
   const uint32_t lead_uempty = mapa_shared(uempty, 0), lead_tempty = mapa_shared(tempty, 0);
 
@@ -513,16 +531,18 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
         }
         const int half = U.nmma >> 1;  // token rows per CTA
         const int nb = half >> 4;
-        const uint32_t bytes = 2 * (kTileA + nb * kBoxB);  // both CTAs' bytes land on the leader's barrier
-        const int wrow = (2 * U.mt + static_cast<int>(rank)) * 128;
+        const uint32_t bytes = 2 * (MT * kTileA + nb * kBoxB);  // both CTAs' bytes land on the leader's barrier
+        const int wrow = (2 * MT * U.mt + static_cast<int>(rank)) * 128;
         const int trow = U.row0 + static_cast<int>(rank) * half;
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1, 3);
           if (leader) mbar_expect_tx(&full[stage], bytes);
           uint8_t* sa = ring + stage * stage_bytes;
-          tma_load_3d_pair(sa, ma, &full[stage], kb * 64, wrow, U.expert, pol_w);
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+            tma_load_3d_pair(sa + m * kTileA, ma, &full[stage], kb * 64, wrow + 256 * m, U.expert, pol_w);
           for (int j = 0; j < nb; ++j)
-            tma_load_2d_pair(sa + kTileA + j * kBoxB, mb, &full[stage], kb * 64, trow + 16 * j, pol_act);
+            tma_load_2d_pair(sa + MT * kTileA + j * kBoxB, mb, &full[stage], kb * 64, trow + 16 * j, pol_act);
           if (++stage == nstages) {
             stage = 0;
             phase ^= 1;
@@ -548,16 +568,20 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
         const uint32_t idesc = idesc_bf16_f32(256, U.nmma);
         mbar_wait_cluster(&tempty[acc], aphase ^ 1, 5);
         tc_fence_after();
-        const uint32_t dt = tmem_base + static_cast<uint32_t>(acc * BN);
+        const uint32_t dt = tmem_base + static_cast<uint32_t>(acc * acc_cols);
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&full[stage], phase, 6);
           tc_fence_after();
           const uint32_t sa = smem_u32(ring + stage * stage_bytes);
-          const uint64_t ad = sdesc_kmajor_sw128(sa);
-          const uint64_t bd = sdesc_kmajor_sw128(sa + kTileA);
+          const uint64_t bd = sdesc_kmajor_sw128(sa + MT * kTileA);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide block; +32 B = +2 in the address field
-            umma_bf16_ss_pair(dt, ad + 2 * k, bd + 2 * k, idesc, (kb > U.kb0 || k > 0) ? 1u : 0u);
+          for (int m = 0; m < MT; ++m) {
+            const uint64_t ad = sdesc_kmajor_sw128(sa + m * kTileA);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide block; +32 B = +2 in the address field
+              umma_bf16_ss_pair(dt + static_cast<uint32_t>(m * U.nmma), ad + 2 * k, bd + 2 * k, idesc,
+                                (kb > U.kb0 || k > 0) ? 1u : 0u);
+          }
           umma_commit_pair(&empty[stage]);
           if (++stage == nstages) {
             stage = 0;
@@ -565,8 +589,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
           }
         }
         umma_commit_pair(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) aphase ^= 1;
+        if (++acc == nacc) {
+          acc = 0;
+          aphase ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
@@ -591,24 +617,32 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
       if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
       mbar_wait(&tfull[acc], aphase, 8);
       tc_fence_after();
-      const int tile = 2 * U.mt + static_cast<int>(rank);
-      const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
-      const bool real = tile < (U.phase == 0 ? p.tiles1 : p.tiles2);  // the second tile of an odd count is padding
-      epilogue_store(p, U, tile, real, q, lane, tb);
+      int published = 0;
+#pragma unroll 1
+      for (int m = 0; m < MT; ++m) {
+        const int tile = 2 * (MT * U.mt + m) + static_cast<int>(rank);
+        const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * acc_cols + m * U.nmma) +
+                            (static_cast<uint32_t>(q * 32) << 16);
+        const bool real = tile < (U.phase == 0 ? p.tiles1 : p.tiles2);  // tiles past the end are padding
+        epilogue_store(p, U, tile, real, q, lane, tb);
+        published += real ? 1 : 0;
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if (leader) mbar_arrive(&tempty[acc]);
         else mbar_arrive_cluster(lead_tempty + 8 * acc);
       }
-      if (U.phase == 0 && real) {  // publish this warp's slice of H to phase-1 consumers on other SMs
+      if (U.phase == 0 && published) {  // publish this warp's slices of H to phase-1 consumers on other SMs
         __threadfence();
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, 1);
+        if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, published);
       }
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
+      if (++acc == nacc) {
+        acc = 0;
+        aphase ^= 1;
+      }
     }
   }
   tc_fence_before();
@@ -620,16 +654,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
   }
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int MT>
 static cudaError_t launch_ffn_pair_t(const FfnParams& p, int sm_count, cudaStream_t s) {
   constexpr size_t smem =
-      1024 + STAGES * (kTileA + BN * 64) + (2 * kMaxStages + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
+      1024 + pair_ring_bytes(BN, STAGES, MT) + (2 * kMaxStages + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static int configured_device = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_device != dev) {
-    cudaError_t e = cudaFuncSetAttribute(ffn_pair_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(ffn_pair_kernel<BN, STAGES, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured_device = dev;
@@ -648,7 +682,7 @@ static cudaError_t launch_ffn_pair_t(const FfnParams& p, int sm_count, cudaStrea
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, ffn_pair_kernel<BN, STAGES>, p);
+  return cudaLaunchKernelEx(&cfg, ffn_pair_kernel<BN, STAGES, MT>, p);
 }
 
 // The CTA pair halves each SM's activation tiles but couples two SMs per
@@ -687,6 +721,16 @@ static cudaError_t launch_ffn_t(const FfnParams& p, int sm_count, cudaStream_t s
   return launch_pdl(ffn_kernel<BN, STAGES>, dim3(sm_count), dim3(kFfnThreads), smem, s, p);
 }
 
+// Weight tiles per CTA per stage of the CTA-pair kernel (LYNX_FFN_MT=1/2 A/B switch).
+static int pair_mt() {
+  static int mt = 0;
+  if (!mt) {
+    const char* e = getenv("LYNX_FFN_MT");
+    mt = (e && e[0] == '1' && !e[1]) ? 1 : 2;
+  }
+  return mt;
+}
+
 cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, cudaStream_t s) {
   const bool pair = ffn_use_pair(bn, rows_hint);
   switch (bn) {
@@ -695,9 +739,11 @@ cudaError_t launch_ffn(const FfnParams& p, int bn, int rows_hint, int sm_count, 
     case 64:
       return launch_ffn_t<64, 9>(p, sm_count, s);
     case 128:
-      return pair ? launch_ffn_pair_t<128, 9>(p, sm_count, s) : launch_ffn_t<128, 7>(p, sm_count, s);
+      if (!pair) return launch_ffn_t<128, 7>(p, sm_count, s);
+      return pair_mt() == 2 ? launch_ffn_pair_t<128, 5, 2>(p, sm_count, s) : launch_ffn_pair_t<128, 9, 1>(p, sm_count, s);
     default:
-      return pair ? launch_ffn_pair_t<256, 7>(p, sm_count, s) : launch_ffn_t<256, 4>(p, sm_count, s);
+      if (!pair) return launch_ffn_t<256, 4>(p, sm_count, s);
+      return pair_mt() == 2 ? launch_ffn_pair_t<256, 4, 2>(p, sm_count, s) : launch_ffn_pair_t<256, 7, 1>(p, sm_count, s);
   }
 }
 

@@ -39,12 +39,23 @@ __device__ const double kNpExpLo[16] = {
     -0x1.3b3efbf5e2228p-54,  -0x1.b32dcb94da51dp-56, 0x1.db72fc1f0eab4p-55,  0x1.1affc2b91ce27p-56,
     0x1.c1a7792cb3387p-55,   0x1.36eae30af0cb3p-56,  0x1.4a385a63d07a7p-56,  -0x1.ff7128fd391f0p-55};
 
-__device__ __forceinline__ double np_exp(double x) {
+// The 2^(j/16) table in shared memory: 32 doubles (hi[0..15], lo[0..15]),
+// staged by threads 0..31 before the kernel's griddep_wait, so the cold
+// global load overlaps the predecessor kernel (the caller synchronises).
+__device__ __forceinline__ void np_exp_stage(double* s_tab) {
+  if (threadIdx.x < 32) s_tab[threadIdx.x] = threadIdx.x < 16 ? kNpExpHi[threadIdx.x] : kNpExpLo[threadIdx.x - 16];
+}
+
+// SVML's scalar fallback range (|x| >= 707.7, NaN): out of line, it never
+// runs for softmax arguments of a finite row with spread < 707.
+__device__ __noinline__ double np_exp_rare(double x) { return exp(x); }
+
+__device__ __forceinline__ double np_exp(double x, const double* s_tab) {
   constexpr double kLog2e = 0x1.71547652b82fep+0, kShift = 0x1.8000000003ff0p+48;
   constexpr double kLn2Hi = 0x1.62e42fefa39efp-1, kLn2Lo = 0x1.abc9e3b39803fp-56;
   constexpr double c5 = 0x1.7411836940c04p-10, c4 = 0x1.1101cbbc265c0p-7, c3 = 0x1.55557242d68fep-5;
   constexpr double c2 = 0x1.5555553939732p-3, c1 = 0x1.000000000d008p-1, c0 = 0x1.fffffffffff70p-1;
-  if (!(fabs(x) < 0x1.61da04cbafe44p+9)) return exp(x);
+  if (!(fabs(x) < 0x1.61da04cbafe44p+9)) return np_exp_rare(x);
   const double t = __fma_rz(x, kLog2e, kShift);
   const double n = __dsub_rn(t, kShift);
   const int j = static_cast<int>(__double_as_longlong(t) & 15);
@@ -56,10 +67,13 @@ __device__ __forceinline__ double np_exp(double x) {
   const double s = __fma_rn(c1, r, c0);
   p = __fma_rn(r2, p, q);
   p = __fma_rn(r2, p, s);
-  const double hi = __ldg(&kNpExpHi[j]), lo = __ldg(&kNpExpLo[j]);
+  const double hi = s_tab[j], lo = s_tab[16 + j];
   p = __fma_rn(p, r, lo);
   p = __fma_rn(hi, p, hi);
-  return scalbn(p, static_cast<int>(floor(n)));
+  // 2^floor(n) by exponent arithmetic: p in [1, 2) and the result normal
+  // for |x| < 707.7, so adding to the exponent field is exact (= vscalefpd)
+  const unsigned long long e = static_cast<unsigned long long>(static_cast<long long>(floor(n))) << 52;
+  return __longlong_as_double(static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(p)) + e));
 }
 
 }  // namespace lynx

@@ -437,6 +437,7 @@ __device__ __forceinline__ void batch_policy(const SelectArgs& a, const int32_t*
           better += (cu >= tau && (cu > ct || (cu == ct && u < t))) ? 1 : 0;
         }
         better = __reduce_add_sync(kFull, better);
+        __syncwarp();  // every lane's read of IMP[t] above precedes lane 0's write
         if (lane == 0 && better >= S) IMP[t] |= 2;
       }
       __syncthreads();
@@ -602,11 +603,13 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
   __shared__ int s_keep[LYNX_MAX_EXPERTS];
   __shared__ int s_flags, s_nq, s_clipped;
   __shared__ unsigned long long s_keepmask;
+  __shared__ double s_exp[32];
   extern __shared__ __align__(16) uint8_t s_dyn[];
 
   griddep_launch_dependents();
   const int T = a.T, N = a.N, k = a.k;
   const int t = threadIdx.x;
+  if (a.logits) np_exp_stage(s_exp);
   const bool active = t < T;
   const SelectSmem L = select_smem(T, N, k, true, a.plan.enabled);
   double* CONF = reinterpret_cast<double*>(s_dyn + L.conf);
@@ -621,6 +624,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
   }
   if (t < N) s_icount[t] = 0;
   warm_params(a);
+  __syncthreads();  // s_exp
   SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
   if (a.ep.enabled) {  // peer-memory EP: every rank's logits rows have landed
@@ -648,10 +652,19 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
         }
       if (!finite) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
 #pragma unroll
-      for (int i = 0; i < NT; ++i) p[i] = i < N ? np_exp(p[i] - m) : 0.0;
+#if LYNX_AB_EXP
+      for (int i = 0; i < NT; ++i) p[i] = i < N ? exp(p[i] - m) : 0.0;
+#else
+      for (int i = 0; i < NT; ++i) p[i] = i < N ? np_exp(p[i] - m, s_exp) : 0.0;
+#endif
       const double sum = reg_pairwise_sum<NT>(p, N);
 #pragma unroll
+#if LYNX_AB_DIV
+      const double inv = 1.0 / sum;
+      for (int i = 0; i < NT; ++i) p[i] = p[i] * inv;
+#else
       for (int i = 0; i < NT; ++i) p[i] = p[i] / sum;  // e / s, as numpy divides (router.py:154)
+#endif
       uint64_t taken = ~expert_mask_all(N);
 #pragma unroll 1
       for (int r = 0; r < k; ++r) {
@@ -935,9 +948,11 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   __shared__ int s_flags, s_nq, s_clipped;
   __shared__ unsigned long long s_keepmask;
   __shared__ int s_rlist[LYNX_MAX_EXPERTS];  // retained experts ascending
+  __shared__ double s_exp[32];
   extern __shared__ __align__(16) uint8_t s_dyn[];
 
   griddep_launch_dependents();
+  if (!kGiven) np_exp_stage(s_exp);
   const int T = a.T, N = a.N, k = a.k;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int j = tid & 7, gbase = tid & 24, grp = tid >> 3, ngrp = nthr >> 3;
@@ -957,6 +972,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
   }
   if (tid < N) s_icount[tid] = 0;
   warm_params(a);
+  __syncthreads();  // s_exp
   SEL_TS(0);
   griddep_wait();  // logits come from K0 (programmatic dependent launch)
   if (a.ep.enabled) {  // peer-memory EP: every rank's logits rows have landed
@@ -989,7 +1005,7 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_group(const __gri
       SEL_TS_LOCAL(8);
       if (bad) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
 #pragma unroll
-      for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m) : 0.0;
+      for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m, s_exp) : 0.0;
       SEL_TS_LOCAL(9);
       const double sum = grp_pairwise<EPL>(v, N, j, gbase);
       SEL_TS_LOCAL(10);
@@ -1324,8 +1340,10 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
                                                            double* probs) {
   namespace cg = cooperative_groups;
   __shared__ double zs[LYNX_MAX_EXPERTS];
+  __shared__ double s_exp[32];
   cg::cluster_group cluster = cg::this_cluster();
   griddep_launch_dependents();
+  if (cluster.block_rank() == 0) np_exp_stage(s_exp);  // read by warp 0 after cluster.sync()
   // DSMEM rule: the leader must have started before its shared memory is
   // written.  Arrive now, wait just before the remote store, so the
   // barrier's latency hides behind the dot products.
@@ -1362,7 +1380,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
   m = fmax(m, __shfl_xor_sync(kFull, m, 4));
   bad = __any_sync(kFull, live && bad);
 #pragma unroll
-  for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m) : 0.0;
+  for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m, s_exp) : 0.0;
   const double sum = grp_pairwise<EPL>(v, N, j, gbase);
 #pragma unroll
   for (int q = 0; q < EPL; ++q) v[q] = v[q] / sum;  // e / s, as numpy divides

@@ -1,6 +1,6 @@
 """Device timeline of graphed layer steps (CUPTI via torch.profiler): per
 kernel start/end relative to the step's first kernel, and the gaps.
-    python scripts/timeline.py [--c4] [--tokens T]"""
+    python scripts/timeline.py [--c4 | --c5] [--tokens T]"""
 import json
 import os
 import sys
@@ -16,12 +16,15 @@ def main():
     if "--c4" in sys.argv:
         T, N, k, d, ff, S = 128, 64, 6, 2048, 1408, 2
         pol = L.PolicyConfig(mode="accuracy", freq_keep_budget=16)
+    elif "--c5" in sys.argv:
+        T, N, k, d, ff, S = 256, 8, 2, 6144, 16384, 0
+        pol = L.PolicyConfig(mode="latency", drop_count=4)
     else:
         T, N, k, d, ff, S = 32, 8, 2, 4096, 14336, 0
         pol = L.PolicyConfig(mode="latency", drop_count=4)
     if "--tokens" in sys.argv:
         T = int(sys.argv[sys.argv.index("--tokens") + 1])
-    n = 4
+    n = 3 if "--c5" in sys.argv else 4
     spec = L.MoEModelSpec(n, N, k, d, ff, num_shared_experts=S)
     model = L.build_swiglu_model(spec, seed=0)
     layers = [L.LynxMoELayer(model, l, T, policy=pol) for l in range(n)]
