@@ -85,6 +85,16 @@ int kb2_per_unit(int kb2_total) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// LYNX_FUSED_FRONT=0 runs K0, K1 and K2 as separate kernels for N <= 8 (A/B switch).
+bool fused_front_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LYNX_FUSED_FRONT");
+    v = (e && e[0] == '0' && !e[1]) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // LYNX_ROUTE_IN_K1=1 keeps the routing in K1 for N > 16 (A/B switch).
 bool route_in_k0_enabled() {
   static int v = -1;
@@ -131,6 +141,7 @@ Geometry geometry(const lynx_layer_t* L, int T) {
 
 // Workspace carve-up.  Selection region only for the whole-layer call.
 struct Plan {
+  size_t sync;  // fused-front barrier words (zero before the first call; every call leaves them zero)
   size_t logits, ids, probs, full, conf, counts, retained, assigned, weights, important, flags;
   size_t n_seg, n_used, n_rows, max_rows, seg_expert, seg_row, seg_count, seg_order, perm_token, perm_weight, tok_rows,
       tok_weight;
@@ -151,6 +162,7 @@ Plan plan_for(const lynx_layer_t* L, int T, bool selection) {
     return o;
   };
   if (selection) {
+    p.sync = take(64);
     p.logits = take(sizeof(double) * T * N);
     p.ids = take(sizeof(int32_t) * T * k);
     p.probs = take(sizeof(double) * T * k);
@@ -260,7 +272,7 @@ inline void record(cudaEvent_t const* ev, int i, cudaStream_t s) {
 // N when unknown), for K3's kernel choice only.
 int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_t* out_bf16, float* out_f32,
                    void* ws, const Plan& P, cudaStream_t s, cudaEvent_t const* ev,
-                   const lynx_ep_peers_t* peers = nullptr, int kept_hint = 0) {
+                   const lynx_ep_peers_t* peers = nullptr, int kept_hint = 0, bool gathered = false) {
   const int N = L->num_experts, k = L->top_k, d = L->d_model, ff = L->d_ff, S = L->num_shared;
   const int sms = sm_count_cached();
   if (sms <= 0) return LYNX_ERR_CUDA;
@@ -281,7 +293,7 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   ga.d = d;
   ga.x_perm = at<uint16_t>(ws, P.x_perm);
   record(ev, 0, s);
-  int st = cuda_status(launch_gather(ga, sms, s));
+  int st = gathered ? LYNX_OK : cuda_status(launch_gather(ga, sms, s));  // the fused front gathered already
   if (st) return st;
 
   FfnParams fp{};
@@ -412,10 +424,13 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
 
   const double* logits = given_logits;
   record(ev, 0, stream);
+  // N <= 8, T <= 256 (Mixtral): K0 + K1 + K2 as one fused launch (front_kernel).
+  const bool fused = !logits && N <= 8 && T <= LYNX_SEG_ROWS && layer->num_shared == 0 && fused_front_enabled() &&
+                     front_smem_bytes(T, N, k) <= 48 * 1024;
   // N > 16: the routing itself runs inside K0 (clusters per token) and K1
   // takes the selection as given; N <= 16 keeps it in K1's thread-per-token path.
   const bool route_in_k0 = !logits && N > 16 && route_in_k0_enabled();
-  if (!logits && !route_in_k0) {
+  if (!logits && !route_in_k0 && !fused) {
     double* lg = at<double>(ws, P.logits);
     st = cuda_status(launch_router_logits(hidden, layer->router_wt, T, layer->d_model, N, lg, stream));
     if (st) return st;
@@ -438,6 +453,17 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
 #undef LYNX_PICK
   a.plan = plan_out(ws, P, layer->num_shared);
   a.routed_top = route_in_k0 ? 1 : 0;
+  if (fused) {
+    a.logits = nullptr;
+    st = cuda_status(launch_front(a, hidden, layer->router_wt, layer->d_model, at<uint16_t>(ws, P.x_perm),
+                                  at<int>(ws, P.sync), stream));
+    if (st) return st;
+    record(ev, 1, stream);
+    st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr, nullptr,
+                        kept_hint(policy, decode, N, floor_keep), true);
+    record(ev, 5, stream);
+    return st;
+  }
   if (route_in_k0) {
     st = cuda_status(launch_router_route(hidden, layer->router_wt, T, layer->d_model, N, k, nullptr, a.full, a.ids,
                                          a.probs, stream));

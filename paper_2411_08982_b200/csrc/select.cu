@@ -1403,6 +1403,378 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
   }
 }
 
+// ------------------------------------------- fused front (N <= 8, T <= 256)
+// K0 + K1 + K2 of the layer in ONE launch of T CTAs, one token each, with one
+// grid-wide barrier.  The chain it replaces is a run of latency-bound steps
+// on the critical path before the expert stream can start (router GEMV ->
+// single-CTA selection -> gather); here the per-token steps run on T SMs at
+// once and only the batch-level decisions are global:
+//
+//   A  router logits of token t (RMSNorm fused, router_dots8)
+//   B  softmax (np_exp, numpy's pairwise sum, e / s) + stable top-k +
+//      confidence of token t on warp 0 (lane j = expert j)
+//   -- grid barrier (every CTA resident: K3 may now launch beside us) --
+//   C  the batch policy, computed by every CTA from all tokens' selections
+//      (identical everywhere: integer votes and ranks, the same compares)
+//   D  the remap of every token (thread per token), so each CTA holds the
+//      whole batch's assignment without a second barrier
+//   E  dispatch plan: token t's permuted rows and merged weights, the gather
+//      of its hidden row into them; CTA 0 writes the segment tables.
+//
+// Results are identical to router_logits_kernel + route_select_fast +
+// plan_dispatch + gather_kernel (same arithmetic, same order).  The barrier
+// words (f.sync) must be zero before the first launch; every launch leaves
+// them zero.  Co-residency: the T CTAs only wait for each other (the next
+// kernel's programmatic launch is released after the barrier), and T <= 256
+// small CTAs always fit the 148 SMs.
+struct FrontArgs {
+  SelectArgs s;               // selection outputs + plan (s.logits unused)
+  const uint16_t* hidden;     // [T, d] bf16
+  const uint16_t* router_wt;  // [N, d] bf16
+  int d;
+  uint16_t* x_perm;           // [rows_cap, d] gathered rows
+  int* sync;                  // [4]: barrier arrivals, generation, non-finite flag accumulator (zero)
+};
+
+#ifdef LYNX_TRACE
+#define FRONT_TS(i)                                                                \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ts[24 + (i)] = globaltimer(); \
+  } while (0)
+#else
+#define FRONT_TS(i) (void)0
+#endif
+
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid-wide barrier of the fused front (all CTAs resident, see above):
+// arrivals count up with acquire-release atomics, the last arriver resets
+// the count and publishes the next generation with a release store.
+__device__ __forceinline__ void grid_barrier(int* sync, int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int gen = *reinterpret_cast<volatile int*>(sync + 1);  // read before arriving
+    if (atom_add_acq_rel_gpu(sync, 1) == nblocks - 1) {
+      *reinterpret_cast<volatile int*>(sync) = 0;
+      st_release_gpu(sync + 1, gen + 1);
+    } else {
+      Watchdog wd;
+      while (ld_acquire_gpu(sync + 1) == gen) wd.tick(9);
+    }
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ FrontArgs f) {
+  const SelectArgs& a = f.s;
+  __shared__ double s_exp[32];
+  __shared__ double s_counts[LYNX_MAX_EXPERTS];
+  __shared__ int s_icount[LYNX_MAX_EXPERTS];
+  __shared__ int s_rank[LYNX_MAX_EXPERTS];
+  __shared__ int s_order[LYNX_MAX_EXPERTS];
+  __shared__ int s_keep[LYNX_MAX_EXPERTS];
+  __shared__ int s_cnt[NT], s_base[NT];
+  __shared__ int s_nq, s_clipped;
+  __shared__ int s_flags;
+  __shared__ uint32_t s_keepmask;
+  __shared__ int s_rows[LYNX_MAX_TOPK];
+  __shared__ int s_nrows;
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  const int T = a.T, N = a.N, k = a.k, t = blockIdx.x, tid = threadIdx.x;
+  const int W = (T + 31) >> 5;
+  double* WT = reinterpret_cast<double*>(s_dyn);                            // [T*k] remap weights
+  double* CONF = WT + T * k;                                                  // [T]
+  int32_t* IDS = reinterpret_cast<int32_t*>(CONF + T);                        // [T*k] top-k ids
+  int32_t* ASG = IDS + T * k;                                                 // [T*k] assignments
+  uint32_t* BITS = reinterpret_cast<uint32_t*>(ASG + T * k);                  // [N*W]
+  uint8_t* IMP = reinterpret_cast<uint8_t*>(BITS + N * W);                    // [T]
+  np_exp_stage(s_exp);
+  if (tid < LYNX_MAX_EXPERTS) s_icount[tid] = 0;
+  if (tid == 0) {
+    s_nq = 0;
+    s_clipped = 0;
+    s_flags = 0;
+  }
+  warm_params(f);
+  griddep_wait();  // hidden comes from the previous kernel
+  FRONT_TS(0);
+
+  // A) logits of token t: threads 0..N-1 hold them
+  const double z = router_dots8(f.hidden, f.router_wt, t, f.d, N, 0);
+  FRONT_TS(1);
+
+  // B) softmax + stable top-k + confidence on warp 0, lane j = expert j (the
+  // group layout with one expert per lane: numpy's pairwise sum folds the 8
+  // lanes as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); fewer than 8 add in order)
+  const int j = tid & 7, gbase = tid & 24;
+  double v = 0.0;
+  int ids[LYNX_MAX_TOPK];
+  if (tid < 32) {
+    const bool mine = tid < 8 && j < N;
+    v = mine ? z : (tid < 8 ? -INFINITY : 0.0);  // lanes 8..31 shadow on finite zeros
+    const bool bad = __any_sync(kFull, mine && !isfinite(v));
+    double m = v;
+    m = fmax(m, __shfl_xor_sync(kFull, m, 1));
+    m = fmax(m, __shfl_xor_sync(kFull, m, 2));
+    m = fmax(m, __shfl_xor_sync(kFull, m, 4));
+    double e1[1] = {j < N ? np_exp(v - m, s_exp) : 0.0};
+    const double sum = grp_pairwise<1>(e1, N, j, gbase);
+    v = e1[0] / sum;  // e / s, as numpy divides (router.py:154)
+    if (tid < 8 && j < N) a.full[static_cast<size_t>(t) * N + j] = v;
+    const uint32_t all_l = j < N ? 1u : 0u;
+    uint32_t taken = ~all_l;
+#pragma unroll
+    for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+      if (r >= k) break;
+      double bv;
+      uint32_t cand[1] = {~taken & 1u};
+      double vv[1] = {v};
+      const int b = __shfl_sync(kFull, grp_best<1>(vv, cand[0], j, &bv), 0);  // group 0's pick on every lane
+      if (b == j) taken |= 1u;
+      ids[r] = b;  // warp-uniform: the remap below branches on it around shuffles
+      if (tid == 0) {
+        a.ids[t * k + r] = b;
+        a.probs[t * k + r] = bv;
+      }
+    }
+    double vv[1] = {v}, top1, second;
+    grp_best<1>(vv, all_l, j, &top1);
+    double c = top1;
+    if (a.pol.confidence_metric == LYNX_CONF_MARGIN) {
+      if (N == 1) {
+        c = __shfl_sync(kFull, v, gbase);
+      } else {
+        const int first = grp_best<1>(vv, all_l, j, &top1);
+        grp_best<1>(vv, first == j ? 0u : all_l, j, &second);
+        c = top1 - second;
+      }
+    }
+    if (tid == 0) {
+      a.conf[t] = c;
+      if (bad) atomicOr(f.sync + 2, LYNX_FLAG_NONFINITE);
+    }
+  }
+  FRONT_TS(2);
+  grid_barrier(f.sync, T);
+  griddep_launch_dependents();  // every CTA is resident: the expert FFN may launch now
+  FRONT_TS(3);
+
+  if (t == 0 && tid == 0) {
+    s_flags = f.sync[2];  // every CTA's non-finite report precedes barrier 1
+    f.sync[2] = 0;
+  }
+
+  // C) batch policy (every CTA, identical)
+  const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
+  const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
+  for (int i = tid; i < T * k; i += blockDim.x) IDS[i] = a.ids[i];
+  if (accuracy)
+    for (int i = tid; i < T; i += blockDim.x) CONF[i] = a.conf[i];
+  __syncthreads();
+  if (run_policy) {
+    batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
+  } else if (tid < N) {
+    s_keep[tid] = 1;
+    s_counts[tid] = 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t keep = 0;
+    for (int e = 0; e < N; ++e)
+      if (s_keep[e]) keep |= 1u << e;
+    s_keepmask = keep;
+  }
+  __syncthreads();
+
+  // D) remap of EVERY token (policy.py:171-210), or the identity mask
+  // (policy.py:215-229), thread per token with its probability row in
+  // registers: each CTA then plans the dispatch on its own, with no second
+  // barrier.  The same arithmetic as route_select_fast.
+  const uint32_t keep = s_keepmask;
+#pragma unroll 1
+  for (int u = tid; u < T; u += blockDim.x) {
+    double pr[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) pr[i] = i < N ? a.full[static_cast<size_t>(u) * N + i] : 0.0;
+    double slot_p[LYNX_MAX_TOPK];
+    int asg[LYNX_MAX_TOPK];
+    uint64_t occupied = 0;
+#pragma unroll
+    for (int r = 0; r < LYNX_MAX_TOPK; ++r)
+      if (r < k && ((keep >> IDS[u * k + r]) & 1u)) occupied |= 1ull << IDS[u * k + r];
+#pragma unroll
+    for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+      if (r >= k) break;
+      int e = IDS[u * k + r];
+      if (run_policy && !((keep >> e) & 1u)) {
+        int pick = reg_best<NT>(pr, keep & ~occupied);
+        if (pick < 0) pick = reg_best<NT>(pr, keep);  // collapse (policy.py:197-200)
+        e = pick;
+        occupied |= 1ull << e;
+      }
+      asg[r] = e;
+      slot_p[r] = reg_at<NT>(pr, e);  // full_probs[u, e] (= probs for the identity mask)
+    }
+    const double total = reg_pairwise_sum<LYNX_MAX_TOPK>(slot_p, k);
+    if (run_policy && !(total > 0.0)) atomicOr(&s_flags, LYNX_FLAG_ZERO_MASS);  // CTA 0's copy is written
+#pragma unroll
+    for (int r = 0; r < LYNX_MAX_TOPK; ++r) {
+      if (r >= k) break;
+      ASG[u * k + r] = asg[r];
+      WT[u * k + r] = slot_p[r] / total;  // policy.py:208, 220
+    }
+  }
+  __syncthreads();
+  if (tid < k) {
+    a.assigned[t * k + tid] = ASG[t * k + tid];
+    a.weights[t * k + tid] = WT[t * k + tid];
+  }
+  if (tid == 0 && a.important) a.important[t] = accuracy ? IMP[t] : 0;
+  if (t == 0) {
+    if (tid < N) {
+      if (a.retained) a.retained[tid] = static_cast<uint8_t>(s_keep[tid]);
+      if (a.counts) a.counts[tid] = s_counts[tid];
+    }
+    if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
+  }
+  FRONT_TS(4);
+  FRONT_TS(5);
+
+  // E) dispatch plan (simulator.py:104-112 order) + gather of token t's row
+  const PlanOut& o = a.plan;
+  for (int i = tid; i < N * W; i += blockDim.x) BITS[i] = 0;
+  __syncthreads();
+  for (int i = tid; i < T * k; i += blockDim.x) {
+    const int e = ASG[i];
+    if (e >= 0 && e < N) atomicOr(&BITS[e * W + ((i / k) >> 5)], 1u << ((i / k) & 31));
+  }
+  __syncthreads();
+  if (tid < 32) {
+    // lane e: expert e's row count, 16-padded base (exclusive scan) and the
+    // number of its tokens before t
+    int cnt = 0, below = 0;
+    if (tid < N) {
+      for (int q = 0; q < W; ++q) {
+        const uint32_t word = BITS[tid * W + q];
+        cnt += __popc(word);
+        if (q < (t >> 5)) below += __popc(word);
+        else if (q == (t >> 5)) below += __popc(word & ((1u << (t & 31)) - 1u));
+      }
+    }
+    const int pad = (cnt + 15) & ~15;
+    int incl = pad;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, off);
+      if (tid >= off) incl += y;
+    }
+    const int base = incl - pad;
+    if (tid < N) {
+      s_cnt[tid] = cnt;
+      s_base[tid] = base;
+    }
+    // token t's distinct experts ascending; lane e writes the row of expert e
+    // if t uses it, with the merged weight 0 + its slots on e in slot order
+    // (simulator.py:108-111)
+    uint32_t set = 0;
+    for (int r = 0; r < k; ++r) set |= 1u << ASG[t * k + r];
+    const bool uses = tid < N && ((set >> tid) & 1u);
+    const int slot = __popc(set & ((1u << tid) - 1u));  // position among t's experts
+    if (uses) {
+      double acc = 0.0;
+      for (int r = 0; r < k; ++r)
+        if (ASG[t * k + r] == tid) acc += WT[t * k + r];
+      const float wf = static_cast<float>(acc);
+      const int r0 = base + below;
+      o.tok_rows[t * k + slot] = r0;
+      o.tok_weight[t * k + slot] = wf;
+      o.perm_token[r0] = t;
+      o.perm_weight[r0] = wf;
+      s_rows[slot] = r0;
+    }
+    const int nj = __popc(set);
+    if (tid == 0) s_nrows = nj;
+    if (tid >= nj && tid < k) {
+      o.tok_rows[t * k + tid] = -1;
+      o.tok_weight[t * k + tid] = 0.f;
+    }
+  }
+  __syncthreads();
+  // gather token t's hidden row into each of its permuted rows (K2's work);
+  // padding rows are left as they are: K3 masks every store of a padding token
+  const int nvec = f.d >> 3;
+  const uint4* src = reinterpret_cast<const uint4*>(f.hidden) + static_cast<size_t>(t) * nvec;
+  const int nrows = s_nrows;
+  for (int vv = tid; vv < nvec; vv += blockDim.x) {
+    const uint4 x = src[vv];
+    for (int q = 0; q < nrows; ++q)
+      reinterpret_cast<uint4*>(f.x_perm)[static_cast<size_t>(s_rows[q]) * nvec + vv] = x;
+  }
+  // experts t, t + T, ...: mark their 16-row padding (perm_token = -1)
+  for (int e = t; e < N; e += T) {
+    const int c = s_cnt[e];
+    for (int r = s_base[e] + c + tid; r < s_base[e] + ((c + 15) & ~15); r += blockDim.x) {
+      o.perm_token[r] = -1;
+      o.perm_weight[r] = 0.f;
+    }
+  }
+  if (t == 0) {
+    // segment tables: one segment per used expert (T <= LYNX_SEG_ROWS), queue
+    // order by rows desc then index asc (LPT), scheduler words zeroed
+    for (int i = tid; i < o.n_counters; i += blockDim.x) o.counters[i] = 0;
+    if (tid < 32) {
+      const int c = tid < N ? s_cnt[tid] : 0;
+      const unsigned used = __ballot_sync(kFull, c > 0);
+      const int seg = __popc(used & ((1u << tid) - 1u));  // segment index of expert tid
+      const int nseg = __popc(used);
+      if (c > 0) {
+        o.seg_expert[seg] = tid;
+        o.seg_row[seg] = s_base[tid];
+        o.seg_count[seg] = c;
+        int rank = 0;  // rows desc, segment index asc
+        for (int e2 = 0; e2 < N; ++e2) {
+          const int c2 = s_cnt[e2];
+          const int seg2 = __popc(used & ((1u << e2) - 1u));
+          rank += (c2 > 0 && (c2 > c || (c2 == c && seg2 < seg))) ? 1 : 0;
+        }
+        if (o.seg_order) o.seg_order[rank] = seg;
+      }
+      const int widest = __reduce_max_sync(kFull, static_cast<unsigned>(c));
+      const int nrows = __reduce_add_sync(kFull, static_cast<unsigned>((c + 15) & ~15));
+      if (tid == 0) {
+        if (o.max_rows) *o.max_rows = widest;
+        *o.n_seg = nseg;
+        *o.n_used = nseg;
+        *o.n_rows = nrows;
+      }
+    }
+  }
+  __syncthreads();
+  FRONT_TS(6);
+}
+
+size_t front_smem_bytes(int T, int N, int k) {
+  const int W = (T + 31) >> 5;
+  return sizeof(double) * (static_cast<size_t>(T) * k + T) + 8ull * T * k + 4ull * N * W + T + 16;
+}
+
+cudaError_t launch_front(const SelectArgs& a, const uint16_t* hidden, const uint16_t* router_wt, int d,
+                         uint16_t* x_perm, int* sync, cudaStream_t s) {
+  FrontArgs f{};
+  f.s = a;
+  f.hidden = hidden;
+  f.router_wt = router_wt;
+  f.d = d;
+  f.x_perm = x_perm;
+  f.sync = sync;
+  const size_t smem = front_smem_bytes(a.T, a.N, a.k);
+  if (smem > 48 * 1024) return cudaErrorInvalidValue;
+  return launch_pdl(front_kernel<8>, dim3(a.T), dim3(256), smem, s, f);
+}
+
 // ------------------------------------------------------------- launchers
 cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, double* logits,
                                  cudaStream_t s, const EpLink* put) {

@@ -262,7 +262,8 @@ class LynxMoELayer:
         if workspace is not None and workspace.numel() >= nbytes:
             self.workspace = workspace  # shared by layers that run in stream order
         else:
-            self.workspace = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+            # zero-filled once: the fused front's barrier words start at zero (every call leaves them zero)
+            self.workspace = torch.zeros((nbytes,), dtype=torch.uint8, device="cuda")
         T, N, k = self.T, s.num_experts, s.top_k
         dev = "cuda"
         self.expert_ids = torch.empty((T, k), dtype=torch.int32, device=dev)
