@@ -425,8 +425,8 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   const double* logits = given_logits;
   record(ev, 0, stream);
   // N <= 8, T <= 256 (Mixtral): K0 + K1 + K2 as one fused launch (front_kernel).
-  const bool fused = !logits && N <= 8 && T <= LYNX_SEG_ROWS && layer->num_shared == 0 && fused_front_enabled() &&
-                     front_smem_bytes(T, N, k) <= 48 * 1024;
+  const bool fused = N <= 8 && T <= LYNX_SEG_ROWS && layer->num_shared == 0 && fused_front_enabled() &&
+                     front_smem_bytes(T, N, k, layer->d_model) <= 48 * 1024 && (logits || layer->router_wt);
   // N > 16: the routing itself runs inside K0 (clusters per token) and K1
   // takes the selection as given; N <= 16 keeps it in K1's thread-per-token path.
   const bool route_in_k0 = !logits && N > 16 && route_in_k0_enabled();
@@ -456,7 +456,7 @@ int moe_layer_impl(const lynx_layer_t* layer, const uint16_t* hidden, int T, int
   if (fused) {
     a.logits = nullptr;
     st = cuda_status(launch_front(a, hidden, layer->router_wt, layer->d_model, at<uint16_t>(ws, P.x_perm),
-                                  at<int>(ws, P.sync), stream));
+                                  at<int>(ws, P.sync), logits, stream));
     if (st) return st;
     record(ev, 1, stream);
     st = gather_and_ffn(layer, hidden, T, out, nullptr, ws, P, stream, ev ? ev + 2 : nullptr, nullptr,

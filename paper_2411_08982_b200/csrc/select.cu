@@ -1434,6 +1434,7 @@ struct FrontArgs {
   int d;
   uint16_t* x_perm;           // [rows_cap, d] gathered rows
   int* sync;                  // [4]: barrier arrivals, generation, non-finite flag accumulator (zero)
+  const double* logits_in;    // [T, N] given logits (the decode stack's fused router), or null: phase A
 };
 
 #ifdef LYNX_TRACE
@@ -1502,8 +1503,19 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   griddep_wait();  // hidden comes from the previous kernel
   FRONT_TS(0);
 
+  // token t's hidden row -> shared memory (cp.async), for the gather in E
+  const int nvec = f.d >> 3;
+  uint4* s_row = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(IMP + T) + 15) & ~uintptr_t(15));
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(f.hidden) + static_cast<size_t>(t) * nvec;
+    for (int v4 = tid; v4 < nvec; v4 += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_row + v4)), "l"(src + v4) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+
   // A) logits of token t: threads 0..N-1 hold them
-  const double z = router_dots8(f.hidden, f.router_wt, t, f.d, N, 0);
+  const double z = f.logits_in ? (tid < N ? f.logits_in[static_cast<size_t>(t) * N + tid] : 0.0)
+                               : router_dots8(f.hidden, f.router_wt, t, f.d, N, 0);
   FRONT_TS(1);
 
   // B) softmax + stable top-k + confidence on warp 0, lane j = expert j (the
@@ -1567,6 +1579,12 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
     f.sync[2] = 0;
   }
 
+  // the probability rows of this thread's tokens (remap, D), issued before
+  // the policy so the loads overlap it (T <= 256 = blockDim: one per thread)
+  double pr[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) pr[i] = (tid < T && i < N) ? a.full[static_cast<size_t>(tid) * N + i] : 0.0;
+
   // C) batch policy (every CTA, identical)
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
   const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
@@ -1594,11 +1612,8 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   // registers: each CTA then plans the dispatch on its own, with no second
   // barrier.  The same arithmetic as route_select_fast.
   const uint32_t keep = s_keepmask;
-#pragma unroll 1
-  for (int u = tid; u < T; u += blockDim.x) {
-    double pr[NT];
-#pragma unroll
-    for (int i = 0; i < NT; ++i) pr[i] = i < N ? a.full[static_cast<size_t>(u) * N + i] : 0.0;
+  if (tid < T) {
+    const int u = tid;
     double slot_p[LYNX_MAX_TOPK];
     int asg[LYNX_MAX_TOPK];
     uint64_t occupied = 0;
@@ -1703,13 +1718,14 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
     }
   }
   __syncthreads();
-  // gather token t's hidden row into each of its permuted rows (K2's work);
-  // padding rows are left as they are: K3 masks every store of a padding token
-  const int nvec = f.d >> 3;
-  const uint4* src = reinterpret_cast<const uint4*>(f.hidden) + static_cast<size_t>(t) * nvec;
+  // gather token t's hidden row (staged in shared memory by cp.async at the
+  // start) into each of its permuted rows -- K2's work; padding rows are left
+  // as they are: K3 masks every store of a padding token
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   const int nrows = s_nrows;
   for (int vv = tid; vv < nvec; vv += blockDim.x) {
-    const uint4 x = src[vv];
+    const uint4 x = s_row[vv];
     for (int q = 0; q < nrows; ++q)
       reinterpret_cast<uint4*>(f.x_perm)[static_cast<size_t>(s_rows[q]) * nvec + vv] = x;
   }
@@ -1756,13 +1772,13 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   FRONT_TS(6);
 }
 
-size_t front_smem_bytes(int T, int N, int k) {
+size_t front_smem_bytes(int T, int N, int k, int d) {
   const int W = (T + 31) >> 5;
-  return sizeof(double) * (static_cast<size_t>(T) * k + T) + 8ull * T * k + 4ull * N * W + T + 16;
+  return sizeof(double) * (static_cast<size_t>(T) * k + T) + 8ull * T * k + 4ull * N * W + T + 16 + 2ull * d + 16;
 }
 
 cudaError_t launch_front(const SelectArgs& a, const uint16_t* hidden, const uint16_t* router_wt, int d,
-                         uint16_t* x_perm, int* sync, cudaStream_t s) {
+                         uint16_t* x_perm, int* sync, const double* logits_in, cudaStream_t s) {
   FrontArgs f{};
   f.s = a;
   f.hidden = hidden;
@@ -1770,7 +1786,8 @@ cudaError_t launch_front(const SelectArgs& a, const uint16_t* hidden, const uint
   f.d = d;
   f.x_perm = x_perm;
   f.sync = sync;
-  const size_t smem = front_smem_bytes(a.T, a.N, a.k);
+  f.logits_in = logits_in;
+  const size_t smem = front_smem_bytes(a.T, a.N, a.k, d);
   if (smem > 48 * 1024) return cudaErrorInvalidValue;
   return launch_pdl(front_kernel<8>, dim3(a.T), dim3(256), smem, s, f);
 }
