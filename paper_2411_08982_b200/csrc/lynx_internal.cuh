@@ -188,6 +188,7 @@ cudaError_t launch_router_route(const uint16_t* hidden, const uint16_t* wt, int 
                                 double* logits, double* full, int32_t* ids, double* probs, cudaStream_t s);
 // Fused K0 + K1 + K2 for N <= 8, T <= 256, no shared experts (select.cu front_kernel).
 size_t front_smem_bytes(int T, int N, int k, int d);
+
 cudaError_t launch_front(const SelectArgs& a, const uint16_t* hidden, const uint16_t* router_wt, int d,
                          uint16_t* x_perm, int* sync, const double* logits_in, cudaStream_t s);
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan);

@@ -1,14 +1,18 @@
 #!/bin/bash
-# ncu evidence for one round: launch list of the default bench (C2) and one
-# full capture of the expert GEMM (K3) -> gpurun_out/
+# ncu evidence for one round -> gpurun_out/: launch lists of C2 / C4 / C5 and
+# --set full captures of K3 at C2 (ffn_kernel) and C5 T=256 (ffn_pair_kernel)
+# plus the C2 front / combine kernels
 mkdir -p gpurun_out
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-echo "launches rc=$?"
+B="python bench.py --warmup 3 --no-cpu-baseline"
+for cfg in c2 c4 c5; do
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+    --log-file gpurun_out/launches_$cfg.csv $B --steps 20 --config $cfg > /dev/null 2>&1
+  echo "launches $cfg rc=$?"
+done
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ffn_kernel -s 6 -c 1 \
-  -o gpurun_out/ffn_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-echo "full rc=$?"
-timeout 900 ncu --set full --clock-control none -k regex:"route_select|router_logits|gather_kernel|combine_kernel" -s 8 -c 4 \
-  -o gpurun_out/small_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-echo "small rc=$?"
-ls -la gpurun_out/
+  -o gpurun_out/ffn_full $B --steps 3 --config c2 > /dev/null 2>&1; echo "ffn c2 rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ffn_pair_kernel -s 3 -c 1 \
+  -o gpurun_out/ffn_pair_full $B --steps 3 --config c5 > /dev/null 2>&1; echo "ffn pair c5 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"front_kernel|combine_kernel" -s 8 -c 2 \
+  -o gpurun_out/small_full $B --steps 3 --config c2 > /dev/null 2>&1; echo "small rc=$?"
+ls -la gpurun_out/*.ncu-rep

@@ -52,7 +52,7 @@ def main():
     ev.sort(key=lambda e: e.time_range.start)
     steps, cur = [], []
     for e in ev:
-        if ("router_" in e.name or "front_kernel" in e.name) and cur:  # K0 (router_logits_kernel, router_route_kernel) or the fused front
+        if ("router_" in e.name or "front_" in e.name) and cur:  # K0 (router_logits_kernel, router_route_kernel) or the fused front
             steps.append(cur)
             cur = []
         cur.append(e)

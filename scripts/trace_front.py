@@ -18,9 +18,10 @@ def main():
     lib = nat.lib()
     lib.lynx_debug_select_ts.argtypes = [ctypes.c_void_p]
     T, d, ff = (256, 6144, 16384) if "--c5" in sys.argv else (32, 4096, 14336)
-    spec = L.MoEModelSpec(2, 8, 2, d, ff)
-    model = L.build_swiglu_model(spec, seed=0)
+    N, k, S = 8, 2, 0
     cfg = L.PolicyConfig(mode="latency", drop_count=4)
+    spec = L.MoEModelSpec(2, N, k, d, ff, num_shared_experts=S)
+    model = L.build_swiglu_model(spec, seed=0)
     layers = [L.LynxMoELayer(model, l, T, policy=cfg) for l in range(2)]
     h = torch.randn((T, d), device="cuda").to(torch.bfloat16)
     rows = []
