@@ -17,6 +17,7 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+           "lts__t_sectors_srcunit_tex_op_read.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
            "launch__shared_mem_per_block", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]
@@ -28,8 +29,11 @@ def short(name):
     return re.sub(r"\(int\)|\(bool\)", "", name)
 
 
-def launches(tag):
-    rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
+def launches(tag, cfg):
+    path = os.path.join(OUT, f"launches_{cfg}.csv")
+    if not os.path.exists(path):
+        return
+    rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
     ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
@@ -38,14 +42,14 @@ def launches(tag):
         if len(r) > vi and r[mi] == "gpu__time_duration.sum" and "lynx::" in r[ki]:
             per[short(r[ki])].append(float(r[vi].replace(",", "")) / 1e3)  # ns -> us
     tot = sum(sum(v) for v in per.values())
-    lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none), round {tag[1:]}",
+    lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none), round {tag[1:]}, config {cfg}",
              "# command: ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv python bench.py "
-             "--steps 20 --warmup 3 --no-cpu-baseline",
+             f"--steps 20 --warmup 3 --no-cpu-baseline --config {cfg}  (scripts/ncu_round.sh)",
              "# cold-cache, serialised replays: compare SHARES of the step, not absolutes",
              f"{'kernel':40s} {'launches':>9s} {'mean_us':>9s} {'min_us':>9s} {'share':>7s}"]
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k:40s} {len(v):9d} {sum(v) / len(v):9.2f} {min(v):9.2f} {100 * sum(v) / tot:6.1f}%")
-    open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(PROF, f"{tag}_launches_{cfg}.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
@@ -69,31 +73,42 @@ def to_bytes(s):
     return float(v.replace(",", "")) * UNIT[u]
 
 
+CAPTURES = [  # (report in gpurun_out/, what it holds)
+    ("ffn_full.ncu-rep", "C2 (Mixtral-8x7B layer, T=32, latency drop 4): ffn_kernel"),
+    ("ffn_pair_full.ncu-rep", "C5 (Mixtral-8x22B layer, T=256, latency drop 4): ffn_pair_kernel (MT=2)"),
+    ("small_full.ncu-rep", "C2: fused front_kernel (K0+K1+K2) and combine_kernel (K4)"),
+    ("r02_ffn_c4.ncu-rep", "C4 (DeepSeek-MoE-16B, T=128, accuracy budget 16): ffn_kernel"),
+    ("r02_k01_c4.ncu-rep", "C4: router_route_kernel (K0 + routing) and route_select_group (K1)"),
+]
+
+
 def main():
-    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
     for f in sorted(os.listdir(OUT)):
         if f.startswith("bench_") and f.endswith(".json") and os.path.getsize(os.path.join(OUT, f)):
             shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
-    for f in ("timeline_c2.json", "timeline_c4.json"):
+    for f in ("timeline_c2.json", "timeline_c4.json", "timeline_c5.json"):
         if os.path.exists(os.path.join(OUT, f)) and os.path.getsize(os.path.join(OUT, f)):
             shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
     if os.path.exists(os.path.join(OUT, "timeline_stack.json")):
         shutil.copy(os.path.join(OUT, "timeline_stack.json"), os.path.join(PROF, f"{tag}_timeline_stack_c3.json"))
-    launches(tag)
+    for cfg in ("c2", "c4", "c5"):
+        launches(tag, cfg)
     kernels = []
-    for rep in ("ffn_full.ncu-rep", "small_full.ncu-rep"):
+    for rep, what in CAPTURES:
         if os.path.exists(os.path.join(OUT, rep)):
-            kernels += ncu_raw(os.path.join(OUT, rep))
-    shutil.copy(os.path.join(OUT, "ffn_full.ncu-rep"), os.path.join(PROF, f"{tag}_ffn_full.ncu-rep"))
+            for k in ncu_raw(os.path.join(OUT, rep)):
+                k["capture"] = what
+                kernels.append(k)
     summary = {
-        "what": "ncu --set full --clock-control none captures of one C2 layer step (Mixtral-8x7B shape, T=32, "
-                "Lynx latency drop 4, 4 used experts)",
-        "commands": ["scripts/ncu_round.sh"],
-        "note": "per-kernel times are cold-cache replays; ffn_kernel DRAM read vs 1.409 GB algorithmic "
-                "(4 x 3*d*ff*2): only the used experts are streamed, each once",
+        "what": "ncu --set full --clock-control none captures, round " + tag[1:],
+        "commands": ["scripts/ncu_round.sh", "scripts/ncu_r02.sh (C4 captures)"],
+        "note": "per-kernel times are cold-cache serialised replays; dram__bytes_read vs the algorithmic "
+                "used-expert bytes shows each used expert streamed once; lts__t_sectors_srcunit_tex_op_read x 32 B "
+                "= the L2 -> SM bytes (weights + activation tiles)",
         "kernels": kernels}
     json.dump(summary, open(os.path.join(PROF, f"{tag}_ncu_full_summary.json"), "w"), indent=1)
-    ffn = next(k for k in kernels if "ffn_kernel" in k["Kernel Name"])
+    ffn = next(k for k in kernels if "ffn_kernel" in k["Kernel Name"] and "C2" in k["capture"])
     rd, wr = to_bytes(ffn["dram__bytes_read.sum"]), to_bytes(ffn["dram__bytes_write.sum"])
     json.dump({"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                "source": f"ncu --set full, profiles/{tag}_ncu_full_summary.json (ffn_kernel, C2 Lynx drop 4, "
@@ -105,12 +120,20 @@ def main():
     ops = collections.Counter(m.group(1) for m in re.finditer(r"/\*[0-9a-f]{4,}\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Za-z0-9_.]+)",
                                                                sass))
     keep = {o: c for o, c in ops.items() if re.match(r"UTC|UTMA|LDTM|SYNCS|HMMA", o)}
-    lines = [f"# SASS evidence (cuobjdump -sass build/ffn.o, all ffn_kernel<BN,STAGES> instances), round {tag[1:]}",
-             "# tcgen05.mma -> UTCHMMA, tcgen05.ld -> LDTM, TMA -> UTMALDG, mbarriers -> SYNCS; "
+    lines = [f"# SASS evidence (cuobjdump -sass build/ffn.o, all ffn_kernel / ffn_pair_kernel instances), round {tag[1:]}",
+             "# tcgen05.mma -> UTCHMMA (.2CTA = cta_group::2), tcgen05.ld -> LDTM, TMA -> UTMALDG, mbarriers -> SYNCS; "
              "no HMMA (legacy mma.sync) anywhere"]
     lines += [f"{c:7d} {o}" for o, c in sorted(keep.items(), key=lambda kv: -kv[1])]
     open(os.path.join(PROF, f"{tag}_sass_evidence.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
+    # compute-sanitizer summary lines
+    san = [ln for tool in ("memcheck", "racecheck", "synccheck", "initcheck")
+           for ln in open(os.path.join(OUT, f"sanitize_{tool}.log")).read().splitlines()
+           if "SUMMARY" in ln] if os.path.exists(os.path.join(OUT, "sanitize_memcheck.log")) else []
+    if san:
+        open(os.path.join(PROF, f"{tag}_sanitize_summary.txt"), "w").write(
+            "# compute-sanitizer over scripts/sanitize.py (all cases), tools memcheck racecheck synccheck initcheck\n"
+            + "\n".join(san) + "\n")
 
 
 if __name__ == "__main__":
