@@ -1326,44 +1326,135 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const uint16_t* __re
   }
 }
 
+// router_dots8 for TPC tokens at once (rows t0 .. t0+TPC-1, clamped): every
+// weight vector loaded is reused for all TPC tokens, so the CTAs of a routing
+// cluster re-read the router TPC times less.  Per token the arithmetic is
+// router_dots8's (same per-thread column walk, same reduction order): the
+// same bits.  Threads 0..7 return z[q] for expert n0 + tid of token t0 + q.
+template <int TPC>
+__device__ __forceinline__ void router_dots8_multi(const uint16_t* __restrict__ hidden,
+                                                   const uint16_t* __restrict__ wt, int t0, int T, int d, int N,
+                                                   int n0, double (&z)[TPC]) {
+  const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(wt);
+  float acc[TPC][8];
+  float ss[TPC];
+#pragma unroll
+  for (int q = 0; q < TPC; ++q) {
+    ss[q] = 0.f;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) acc[q][n] = 0.f;
+  }
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    uint4 wv[8];
+    uint4 hv[TPC];
+#pragma unroll
+    for (int q = 0; q < TPC; ++q) {
+      const int t = min(t0 + q, T - 1);
+      hv[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(hidden) +
+                                              static_cast<size_t>(t) * d + c);
+    }
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int e = min(n0 + n, N - 1);
+      wv[n] = __ldg(reinterpret_cast<const uint4*>(w + static_cast<size_t>(e) * d + c));
+    }
+#pragma unroll
+    for (int q = 0; q < TPC; ++q) {
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv[q]);
+      float hf[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h2[j]);
+        hf[2 * j] = f.x;
+        hf[2 * j + 1] = f.y;
+        ss[q] += f.x * f.x + f.y * f.y;
+      }
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[n]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(w2[j]);
+          acc[q][n] += hf[2 * j] * f.x + hf[2 * j + 1] * f.y;
+        }
+      }
+    }
+  }
+  __shared__ float s_red[8][TPC][9];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < TPC; ++q)
+#pragma unroll
+    for (int n = 0; n < 9; ++n) {
+      float v = n < 8 ? acc[q][n] : ss[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if (lane == 0) s_red[warp][q][n] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < 9 * TPC) {
+    const int q = threadIdx.x / 9, n = threadIdx.x % 9;
+    float v = 0.f;
+    for (int i = 0; i < 8; ++i) v += s_red[i][q][n];
+    s_red[0][q][n] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < TPC; ++q) {
+    z[q] = 0.0;
+    if (threadIdx.x < 8) {
+      const double inv = 1.0 / sqrt(static_cast<double>(s_red[0][q][8]) / d + 1e-12);
+      z[q] = static_cast<double>(s_red[0][q][threadIdx.x]) * inv;
+    }
+  }
+}
+
 // K0 with the routing folded in (router.py:141-187), for 16 < N <= 64.  A
-// cluster of ceil(N/8) CTAs per token computes the token's logits (8 experts
-// per CTA, router_dots8) into the cluster leader's shared memory (DSMEM);
-// after one cluster barrier the leader's first eight lanes run the group
-// path's softmax (numpy pairwise sum) + stable top-k for the token.  The
-// softmax over 64 experts of 128 tokens then spreads over 128 SMs instead of
-// one (K1 is a single CTA), and K1 runs on the given selection.  Rows with
-// non-finite logits are written as NaN so K1 raises LYNX_FLAG_NONFINITE.
+// cluster of ceil(N/8) CTAs per group of TPC tokens computes their logits
+// (8 experts per CTA, router_dots8_multi) into the cluster leader's shared
+// memory (DSMEM); after one cluster barrier the leader's warp 0 routes the
+// tokens, eight lanes each (the group path's softmax with numpy's pairwise
+// sum + stable top-k), four tokens per warp.  The softmax over 64 experts of
+// 128 tokens then spreads over many SMs instead of K1's one, and K1 runs on
+// the given selection.  Rows with non-finite logits are written as NaN so K1
+// raises LYNX_FLAG_NONFINITE.
+template <int TPC>
 __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __restrict__ hidden,
-                                                           const uint16_t* __restrict__ wt, int d, int N, int k,
-                                                           double* logits, double* full, int32_t* ids,
+                                                           const uint16_t* __restrict__ wt, int T, int d, int N,
+                                                           int k, double* logits, double* full, int32_t* ids,
                                                            double* probs) {
   namespace cg = cooperative_groups;
-  __shared__ double zs[LYNX_MAX_EXPERTS];
+  static_assert(TPC <= 4, "four tokens per routing warp");
+  __shared__ double zs[TPC][LYNX_MAX_EXPERTS];
   __shared__ double s_exp[32];
   cg::cluster_group cluster = cg::this_cluster();
   griddep_launch_dependents();
-  if (cluster.block_rank() == 0) np_exp_stage(s_exp);  // read by warp 0 after cluster.sync()
   // DSMEM rule: the leader must have started before its shared memory is
   // written.  Arrive now, wait just before the remote store, so the
   // barrier's latency hides behind the dot products.
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  const int t = blockIdx.y, c = static_cast<int>(cluster.block_rank());
+  const int t0 = blockIdx.y * TPC, c = static_cast<int>(cluster.block_rank());
   const int n0 = c * 8;
+  if (c == 0) np_exp_stage(s_exp);  // read by warp 0 after cluster.sync()
   griddep_wait();  // hidden may be produced by the previous kernel
-  const double z = router_dots8(hidden, wt, t, d, N, n0);
+  double z[TPC];
+  router_dots8_multi<TPC>(hidden, wt, t0, T, d, N, n0, z);
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
-    double* zl = cluster.map_shared_rank(zs, 0);
-    zl[n0 + threadIdx.x] = z;
-    if (logits) logits[static_cast<size_t>(t) * N + n0 + threadIdx.x] = z;
+#pragma unroll
+    for (int q = 0; q < TPC; ++q) {
+      double* zl = cluster.map_shared_rank(&zs[q][0], 0);
+      zl[n0 + threadIdx.x] = z[q];
+      if (logits && t0 + q < T) logits[static_cast<size_t>(t0 + q) * N + n0 + threadIdx.x] = z[q];
+    }
   }
   cluster.sync();
   if (c != 0 || threadIdx.x >= 32) return;
-  // warp 0 of the leader: lanes 0..7 route token t (group 0); the other
-  // groups of the warp shadow it on zeros (shuffles stay warp-converged)
-  const int j = threadIdx.x & 7, gbase = threadIdx.x & 24;
-  const bool live = threadIdx.x < 8;
+  // warp 0 of the leader: group g = lanes 8g..8g+7 routes token t0 + g; the
+  // groups past TPC (or past T) shadow on zeros (shuffles stay warp-converged)
+  const int j = threadIdx.x & 7, gbase = threadIdx.x & 24, g = threadIdx.x >> 3;
+  const int t = t0 + g;
+  const bool live = g < TPC && t < T;
   constexpr int EPL = 8;
   double v[EPL];
   bool bad = false;
@@ -1371,14 +1462,15 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
 #pragma unroll
   for (int q = 0; q < EPL; ++q) {
     const int e = j + 8 * q;
-    v[q] = e < N ? (live ? zs[e] : 0.0) : -INFINITY;
+    v[q] = e < N ? (live ? zs[g < TPC ? g : 0][e] : 0.0) : -INFINITY;
     if (e < N) bad |= !isfinite(v[q]);
     m = v[q] > m ? v[q] : m;
   }
   m = fmax(m, __shfl_xor_sync(kFull, m, 1));
   m = fmax(m, __shfl_xor_sync(kFull, m, 2));
   m = fmax(m, __shfl_xor_sync(kFull, m, 4));
-  bad = __any_sync(kFull, live && bad);
+  const unsigned badg = __ballot_sync(kFull, live && bad);
+  bad = (badg >> gbase) & 0xffu;  // any lane of this token's group
 #pragma unroll
   for (int q = 0; q < EPL; ++q) v[q] = (j + 8 * q < N) ? np_exp(v[q] - m, s_exp) : 0.0;
   const double sum = grp_pairwise<EPL>(v, N, j, gbase);
@@ -1803,8 +1895,10 @@ cudaError_t launch_router_logits(const uint16_t* hidden, const uint16_t* wt, int
 cudaError_t launch_router_route(const uint16_t* hidden, const uint16_t* wt, int T, int d, int N, int k,
                                 double* logits, double* full, int32_t* ids, double* probs, cudaStream_t s) {
   const int cl = (N + 7) / 8;
+  // tokens per cluster: 4 once there are enough tokens to keep the SMs busy
+  const int tpc = T >= 64 ? 4 : 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cl, T);
+  cfg.gridDim = dim3(cl, (T + tpc - 1) / tpc);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
@@ -1817,7 +1911,8 @@ cudaError_t launch_router_route(const uint16_t* hidden, const uint16_t* wt, int 
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, router_route_kernel, hidden, wt, d, N, k, logits, full, ids, probs);
+  if (tpc == 4) return cudaLaunchKernelEx(&cfg, router_route_kernel<4>, hidden, wt, T, d, N, k, logits, full, ids, probs);
+  return cudaLaunchKernelEx(&cfg, router_route_kernel<1>, hidden, wt, T, d, N, k, logits, full, ids, probs);
 }
 
 size_t select_smem_bytes(int T, int N, int k, bool stage, bool plan) {
