@@ -652,19 +652,10 @@ __global__ void __launch_bounds__(kSelectThreads) route_select_fast(const __grid
         }
       if (!finite) atomicOr(&s_flags, LYNX_FLAG_NONFINITE);
 #pragma unroll
-#if LYNX_AB_EXP
-      for (int i = 0; i < NT; ++i) p[i] = i < N ? exp(p[i] - m) : 0.0;
-#else
       for (int i = 0; i < NT; ++i) p[i] = i < N ? np_exp(p[i] - m, s_exp) : 0.0;
-#endif
       const double sum = reg_pairwise_sum<NT>(p, N);
 #pragma unroll
-#if LYNX_AB_DIV
-      const double inv = 1.0 / sum;
-      for (int i = 0; i < NT; ++i) p[i] = p[i] * inv;
-#else
       for (int i = 0; i < NT; ++i) p[i] = p[i] / sum;  // e / s, as numpy divides (router.py:154)
-#endif
       uint64_t taken = ~expert_mask_all(N);
 #pragma unroll 1
       for (int r = 0; r < k; ++r) {
@@ -1680,24 +1671,61 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   // C) batch policy (every CTA, identical)
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
   const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
-  for (int i = tid; i < T * k; i += blockDim.x) IDS[i] = a.ids[i];
-  if (accuracy)
-    for (int i = tid; i < T; i += blockDim.x) CONF[i] = a.conf[i];
-  __syncthreads();
-  if (run_policy) {
-    batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
-  } else if (tid < N) {
-    s_keep[tid] = 1;
-    s_counts[tid] = 0.0;
+  if (run_policy && !accuracy && a.pol.n_rank_weights == 0 && T * k <= 256) {
+    // latency_policy with unit votes on warp 0 alone (policy.py:116-148,
+    // 232-264): ballots count each expert's slots, lane e ranks expert e by
+    // (count desc, index asc) against the others, the first N - eff are kept.
+    // Integer arithmetic: the same decisions as batch_policy, no block barrier.
+    if (tid < 32) {
+      int cnt = 0;
+      for (int i0 = 0; i0 < T * k; i0 += 32) {
+        const int i = i0 + tid;
+        const int id = i < T * k ? a.ids[i] : -1;
+        if (i < T * k) IDS[i] = id;
+        for (int e = 0; e < N; ++e) {
+          const unsigned m = __ballot_sync(kFull, id == e);
+          if (tid == e) cnt += __popc(m);
+        }
+      }
+      int rank = 0;
+      for (int f = 0; f < N; ++f) {
+        const int cf = __shfl_sync(kFull, cnt, f);
+        rank += (cf > cnt || (cf == cnt && f < tid)) ? 1 : 0;
+      }
+      const int room = N - a.floor_keep > 0 ? N - a.floor_keep : 0;
+      const int eff = a.pol.drop_count < room ? a.pol.drop_count : room;
+      const bool kept = tid < N && rank < N - eff;
+      const unsigned km = __ballot_sync(kFull, kept);
+      if (tid < N) {
+        s_keep[tid] = kept ? 1 : 0;
+        s_counts[tid] = static_cast<double>(cnt);
+      }
+      if (tid == 0) {
+        s_keepmask = km;
+        s_clipped = eff != a.pol.drop_count;
+      }
+    }
+    __syncthreads();
+  } else {
+    for (int i = tid; i < T * k; i += blockDim.x) IDS[i] = a.ids[i];
+    if (accuracy)
+      for (int i = tid; i < T; i += blockDim.x) CONF[i] = a.conf[i];
+    __syncthreads();
+    if (run_policy) {
+      batch_policy(a, IDS, CONF, IMP, s_keep, s_counts, s_icount, s_rank, s_order, &s_nq, &s_clipped);
+    } else if (tid < N) {
+      s_keep[tid] = 1;
+      s_counts[tid] = 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t keep = 0;
+      for (int e = 0; e < N; ++e)
+        if (s_keep[e]) keep |= 1u << e;
+      s_keepmask = keep;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t keep = 0;
-    for (int e = 0; e < N; ++e)
-      if (s_keep[e]) keep |= 1u << e;
-    s_keepmask = keep;
-  }
-  __syncthreads();
 
   // D) remap of EVERY token (policy.py:171-210), or the identity mask
   // (policy.py:215-229), thread per token with its probability row in
@@ -1748,10 +1776,52 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
     if (tid == 0) a.flags[0] = s_flags | (s_clipped ? LYNX_FLAG_CLIPPED : 0);
   }
   FRONT_TS(4);
-  FRONT_TS(5);
 
   // E) dispatch plan (simulator.py:104-112 order) + gather of token t's row
   const PlanOut& o = a.plan;
+  if (T <= 32) {
+    // one warp, lane u = token u: per expert a ballot of the tokens using it
+    // gives its count and every token's rank among them; the 16-padded bases
+    // accumulate over the experts in order.  No shared bitmap, no barrier.
+    if (tid < 32) {
+      const int u = tid;
+      uint32_t set = 0;
+      if (u < T)
+        for (int r = 0; r < k; ++r) set |= 1u << ASG[u * k + r];
+      int base = 0;
+      for (int e = 0; e < N; ++e) {
+        const bool uses = (set >> e) & 1u;
+        const unsigned m = __ballot_sync(kFull, uses);
+        const int cnt = __popc(m);
+        if (tid == e) {
+          s_cnt[e] = cnt;
+          s_base[e] = base;
+        }
+        if (u == t && uses) {
+          const int slot = __popc(set & ((1u << e) - 1u));
+          double acc = 0.0;  // merged weight: token t's slots on e in slot order (simulator.py:108-111)
+          for (int r = 0; r < k; ++r)
+            if (ASG[t * k + r] == e) acc += WT[t * k + r];
+          const float wf = static_cast<float>(acc);
+          const int r0 = base + __popc(m & ((1u << u) - 1u));
+          o.tok_rows[t * k + slot] = r0;
+          o.tok_weight[t * k + slot] = wf;
+          o.perm_token[r0] = t;
+          o.perm_weight[r0] = wf;
+          s_rows[slot] = r0;
+        }
+        base += (cnt + 15) & ~15;
+      }
+      if (u == t) {
+        const int nj = __popc(set);
+        s_nrows = nj;
+        for (int q = nj; q < k; ++q) {
+          o.tok_rows[t * k + q] = -1;
+          o.tok_weight[t * k + q] = 0.f;
+        }
+      }
+    }
+  } else {
   for (int i = tid; i < N * W; i += blockDim.x) BITS[i] = 0;
   __syncthreads();
   for (int i = tid; i < T * k; i += blockDim.x) {
@@ -1809,10 +1879,12 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
       o.tok_weight[t * k + tid] = 0.f;
     }
   }
+  }
   __syncthreads();
   // gather token t's hidden row (staged in shared memory by cp.async at the
   // start) into each of its permuted rows -- K2's work; padding rows are left
   // as they are: K3 masks every store of a padding token
+  FRONT_TS(5);
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   const int nrows = s_nrows;

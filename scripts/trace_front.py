@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_08982_b200 as L  # noqa: E402
 from paper_2411_08982_b200 import _native as nat  # noqa: E402
 
-NAMES = ["griddep_wait", "A logits", "B softmax/topk", "barrier", "C policy + D remap (all tokens)", "-", "E plan+gather"]
+NAMES = ["griddep_wait", "A logits", "B softmax/topk", "barrier", "C policy + D remap (all tokens)", "E plan",
+         "E gather + tables"]
 
 
 def main():

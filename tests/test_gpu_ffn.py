@@ -421,3 +421,25 @@ def test_cta_pair_kernel_forced_on_every_shape():
                             "random_layer or maximum_sizes or shared_experts or deepseek or swiglu_vs_oracle"],
                            env=env, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, (force, r.stdout[-3000:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("case", ["c2", "acc", "t256", "n5"])
+def test_fused_front_identical_to_kernel_chain(case, tmp_path):
+    """The fused front (K0 + K1 + K2 in one launch, N <= 8) against the
+    K0 -> K1 -> K2 chain (LYNX_FUSED_FRONT=0): every selection output, the
+    flags and the layer output bit for bit, decode and prefill."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for f in ("1", "0"):
+        path = str(tmp_path / f"front{f}.npz")
+        r = subprocess.run([sys.executable, os.path.join(root, "scripts", "front_ab_dump.py"), path, case],
+                           env=dict(os.environ, LYNX_FUSED_FRONT=f), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    a, b = outs
+    assert sorted(a.files) == sorted(b.files)
+    for key in a.files:
+        assert np.array_equal(a[key], b[key]), key
