@@ -55,6 +55,7 @@ constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
 // only needs 16 KB of weights + 2 KB per 16 rows of the widest segment, so a
 // batch whose experts got few rows each runs more stages in the same bytes.
 constexpr int kMaxStages = 12;
+constexpr int kAccSlots = 4;  // TMEM accumulator slots of the CTA-pair kernel
 
 struct Unit {
   int phase, seg, mt, split, kb0, kb1, expert, row0, n, nmma;
@@ -440,9 +441,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
   uint8_t* ring = smem;  // stage s: [MT weight tiles x 16 KB | this CTA's half of the token rows]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRing);
   uint64_t* empty = full + kMaxStages;
-  uint64_t* tfull = empty + kMaxStages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* ufull = tempty + 2;
+  uint64_t* tfull = empty + kMaxStages;  // per accumulator slot (kAccSlots)
+  uint64_t* tempty = tfull + kAccSlots;
+  uint64_t* ufull = tempty + kAccSlots;
   uint64_t* uempty = ufull + kUnitRing;
   int* uring = reinterpret_cast<int*>(uempty + kUnitRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
       mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
       mbar_init(&empty[s], 1);  // multicast MMA commit
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kAccSlots; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);  // leader: 4 epilogue warps x 2 CTAs
     }
@@ -485,8 +486,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
   const int width = p.max_rows ? min(BN, max(32, (*p.max_rows + 31) & ~31)) : BN;
   const int stage_bytes = MT * kTileA + (width >> 1) * 128;
   const int nstages = min(kMaxStages, kRing / stage_bytes);
-  const int nacc = 2 * MT * width <= static_cast<int>(kTmemCols) ? 2 : 1;  // accumulator buffers
-  const int acc_cols = MT * width;  // column stride of the two buffers (2 * MT * width <= 512 when nacc == 2)
+  // TMEM as a ring of `nslot` accumulator slots of `width` columns; unit u's
+  // tile m accumulates in slot (MT u + m) % nslot.  The epilogue frees a
+  // slot as soon as it has drained that tile, so the next unit's MMAs wait
+  // only for the slots they reuse: with 3 slots (width <= 170) the second
+  // tile's drain overlaps the next unit instead of stalling it.
+  const int nslot = min(kAccSlots, static_cast<int>(kTmemCols) / width);
   const uint32_t peer_ufull = mapa_shared(ufull, 1), peer_uring = mapa_shared(uring, 1);
   const uint32_t lead_uempty = mapa_shared(uempty, 0), lead_tempty = mapa_shared(tempty, 0);
 
@@ -553,8 +558,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ------------------------------------------------ MMA issuer (leader only)
-      int stage = 0, slot = 0, acc = 0;
-      uint32_t phase = 0, uphase = 0, aphase = 0;
+      int stage = 0, slot = 0, acc = 0;  // acc: the next accumulator slot
+      uint32_t phase = 0, uphase = 0, aphase = 0;  // aphase: parity bit per accumulator slot
       while (true) {
         mbar_wait(&ufull[slot], uphase, 4);
         const int u = uring[slot];
@@ -566,9 +571,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
         Unit U;
         if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
         const uint32_t idesc = idesc_bf16_f32(256, U.nmma);
-        mbar_wait_cluster(&tempty[acc], aphase ^ 1, 5);
+        int as[MT];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          as[m] = acc;
+          mbar_wait_cluster(&tempty[acc], ((aphase >> acc) & 1u) ^ 1u, 5);
+          if (++acc == nslot) acc = 0;
+        }
         tc_fence_after();
-        const uint32_t dt = tmem_base + static_cast<uint32_t>(acc * acc_cols);
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&full[stage], phase, 6);
           tc_fence_after();
@@ -577,10 +587,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
             const uint64_t ad = sdesc_kmajor_sw128(sa + m * kTileA);
+            const uint32_t dt = tmem_base + static_cast<uint32_t>(as[m] * width);
 #pragma unroll
             for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide block; +32 B = +2 in the address field
-              umma_bf16_ss_pair(dt + static_cast<uint32_t>(m * U.nmma), ad + 2 * k, bd + 2 * k, idesc,
-                                (kb > U.kb0 || k > 0) ? 1u : 0u);
+              umma_bf16_ss_pair(dt, ad + 2 * k, bd + 2 * k, idesc, (kb > U.kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit_pair(&empty[stage]);
           if (++stage == nstages) {
@@ -588,10 +598,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc]);
-        if (++acc == nacc) {
-          acc = 0;
-          aphase ^= 1;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          umma_commit_pair(&tfull[as[m]]);
+          aphase ^= 1u << as[m];
         }
       }
     }
@@ -615,33 +625,30 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
       }
       Unit U;
       if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
-      mbar_wait(&tfull[acc], aphase, 8);
-      tc_fence_after();
       int published = 0;
 #pragma unroll 1
       for (int m = 0; m < MT; ++m) {
+        mbar_wait(&tfull[acc], (aphase >> acc) & 1u, 8);
+        tc_fence_after();
         const int tile = 2 * (MT * U.mt + m) + static_cast<int>(rank);
-        const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * acc_cols + m * U.nmma) +
-                            (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * width) + (static_cast<uint32_t>(q * 32) << 16);
         const bool real = tile < (U.phase == 0 ? p.tiles1 : p.tiles2);  // tiles past the end are padding
         epilogue_store(p, U, tile, real, q, lane, tb);
         published += real ? 1 : 0;
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(&tempty[acc]);
-        else mbar_arrive_cluster(lead_tempty + 8 * acc);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // this slot is free for the next unit's MMAs
+          if (leader) mbar_arrive(&tempty[acc]);
+          else mbar_arrive_cluster(lead_tempty + 8 * acc);
+        }
+        aphase ^= 1u << acc;
+        if (++acc == nslot) acc = 0;
       }
       if (U.phase == 0 && published) {  // publish this warp's slices of H to phase-1 consumers on other SMs
         __threadfence();
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, published);
-      }
-      if (++acc == nacc) {
-        acc = 0;
-        aphase ^= 1;
       }
     }
   }
@@ -656,8 +663,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
 
 template <int BN, int STAGES, int MT>
 static cudaError_t launch_ffn_pair_t(const FfnParams& p, int sm_count, cudaStream_t s) {
-  constexpr size_t smem =
-      1024 + pair_ring_bytes(BN, STAGES, MT) + (2 * kMaxStages + 4 + 2 * kUnitRing) * 8 + kUnitRing * 4 + 16;
+  constexpr size_t smem = 1024 + pair_ring_bytes(BN, STAGES, MT) + (2 * kMaxStages + 2 * kAccSlots + 2 * kUnitRing) * 8 +
+                          kUnitRing * 4 + 16;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   static int configured_device = -1;
   int dev = 0;
