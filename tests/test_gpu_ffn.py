@@ -443,3 +443,57 @@ def test_fused_front_identical_to_kernel_chain(case, tmp_path):
     assert sorted(a.files) == sorted(b.files)
     for key in a.files:
         assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("T", [1, 2, 31, 32, 33, 255, 256])
+def test_fused_front_edge_shapes_vs_oracle(T):
+    """The fused front's edges (N <= 8, T <= 256): one token, a partial warp,
+    exactly one / just over one warp of tokens (the warp-level plan switches
+    at 32), the 256-token limit; N from 1 to 8, k up to N; latency policies
+    with drops past the floor, min_experts and rank weights (the batch_policy
+    path), accuracy policies, prefill.  Selection bit-exact vs the oracle on
+    the kernel's logits, layer output within the bf16 tolerance."""
+    rng = np.random.default_rng(T)
+    for rep in range(6):
+        N = int(rng.choice([1, 2, 5, 7, 8]))
+        k = int(rng.integers(1, N + 1))
+        d, ff = int(rng.choice([64, 128])), int(rng.choice([64, 192]))
+        decode = rep != 5
+        kind = rep % 4
+        if kind == 0:
+            cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 2)))
+            opol = O.Policy(mode="latency", drop_count=cfg.drop_count)
+        elif kind == 1:
+            mk = int(rng.integers(k, N + 1))
+            rw = tuple(float(x) for x in rng.uniform(0.1, 1.0, size=k))
+            cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 1)), min_experts=mk,
+                                 vote_rank_weights=rw)
+            opol = O.Policy(mode="latency", drop_count=cfg.drop_count, min_experts=mk, vote_rank_weights=rw)
+        else:
+            cfg = L.PolicyConfig(mode="accuracy", confidence_threshold=float(rng.choice([0.2, 0.5])),
+                                 sample_threshold=int(rng.integers(1, 10)), freq_keep_budget=int(rng.integers(1, N + 1)),
+                                 confidence_metric=str(rng.choice(["top1", "margin"])))
+            opol = O.Policy(mode="accuracy", confidence_threshold=cfg.confidence_threshold,
+                            sample_threshold=cfg.sample_threshold, freq_keep_budget=cfg.freq_keep_budget,
+                            confidence_metric=cfg.confidence_metric)
+        model = L.build_swiglu_model(L.MoEModelSpec(1, N, k, d, ff), seed=T * 10 + rep)
+        g = torch.Generator(device="cuda").manual_seed(rep)
+        hidden = torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16)
+        layer = L.LynxMoELayer(model, 0, T, policy=cfg, phase=L.Phase.DECODE if decode else L.Phase.PREFILL)
+        y = layer(hidden)
+        torch.cuda.synchronize()
+        logits = _np(L.router_logits(model, 0, hidden))
+        ids, probs, full = O.route(logits, k)
+        ref_mask = O.apply(ids, probs, full, opol, decode=decode)
+        tag = dict(T=T, N=N, k=k, rep=rep, decode=decode, cfg=cfg)
+        assert np.array_equal(_np(layer.expert_ids), ids), tag
+        assert np.array_equal(_np(layer.assigned), ref_mask.assigned), tag
+        keep = np.zeros(N, dtype=np.uint8)
+        keep[ref_mask.retained] = 1
+        assert np.array_equal(_np(layer.retained_mask), keep), tag
+        assert np.allclose(_np(layer.weights), ref_mask.weights, rtol=1e-12, atol=1e-15), tag
+        assert bool(int(layer.flags.item()) & 1) == bool(ref_mask.clipped), tag
+        w1, w3 = L.unpack_w13(model.w13[0], ff)
+        f = lambda t: t.float().cpu().numpy()  # noqa: E731
+        ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights)
+        assert O.norm_rel_err(_np(y), ref) <= TOL, tag
