@@ -47,6 +47,10 @@
 namespace lynx {
 
 constexpr int kFfnThreads = 256;
+// CTA-pair kernel: 12 warps, epilogue warps 4..11 = two per TMEM lane
+// quarter, each draining half of a tile's token columns
+constexpr int kPairThreads = 384;
+constexpr int kPairEpiWarps = 8;
 constexpr int kUnitRing = 4;
 constexpr int kTileA = 128 * 64 * 2;  // 128 weight rows x 64 bf16 (one 128B-swizzled k block)
 constexpr int kBoxB = 16 * 64 * 2;    // 16 token rows x 64 bf16
@@ -124,14 +128,14 @@ __device__ __forceinline__ void trace(int role, int id, uint64_t t0, uint64_t t1
 // activation and writes H (bf16); phase 1 writes the split-K partial (f32).
 // `real` = false masks the stores of a padding tile (CTA-pair kernel).
 __device__ __forceinline__ void epilogue_store(const FfnParams& p, const Unit& U, int tile, bool real, int q, int lane,
-                                               uint32_t tb) {
+                                               uint32_t tb, int c_lo, int c_hi) {
   if (U.phase == 0) {
     __nv_bfloat16* H = reinterpret_cast<__nv_bfloat16*>(p.h);
     if (p.act == LYNX_ACT_SWIGLU) {
       // lanes 0-15: gate rows, lanes 16-31: up rows of the same 16 features
       const int f = tile * 64 + q * 16 + (lane & 15);
       const bool upper = lane >= 16;
-      for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+      for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
         uint32_t v[16];
         tmem_ld16(tb + c0, v);
         tmem_ld_wait();
@@ -148,7 +152,7 @@ __device__ __forceinline__ void epilogue_store(const FfnParams& p, const Unit& U
       }
     } else {
       const int f = tile * 128 + q * 32 + lane;
-      for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+      for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
         uint32_t v[16];
         tmem_ld16(tb + c0, v);
         tmem_ld_wait();
@@ -164,7 +168,7 @@ __device__ __forceinline__ void epilogue_store(const FfnParams& p, const Unit& U
     // phase 1: split-K partial for 32 output columns -> slot[s]
     const int r = tile * 128 + q * 32 + lane;
     float* dst = p.partial + (static_cast<size_t>(U.split) * p.rows_cap + U.row0) * p.d + r;
-    for (int c0 = 0; c0 < U.nmma; c0 += 16) {
+    for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
       uint32_t v[16];
       tmem_ld16(tb + c0, v);
       tmem_ld_wait();
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       LYNX_TRACE_T0;
       tc_fence_after();
       const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
-      epilogue_store(p, U, U.mt, true, q, lane, tb);
+      epilogue_store(p, U, U.mt, true, q, lane, tb, 0, U.nmma);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -432,7 +436,7 @@ constexpr int pair_ring_bytes(int BN, int STAGES, int MT) {
 // units' worth fit (N <= 256 / MT), else the epilogue drains one unit while
 // the MMA waits for it.
 template <int BN, int STAGES, int MT>
-__global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_constant__ FfnParams p) {
+__global__ void __launch_bounds__(kPairThreads, 1) ffn_pair_kernel(const __grid_constant__ FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kRing = pair_ring_bytes(BN, STAGES, MT);
@@ -459,11 +463,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
     }
     for (int i = 0; i < kAccSlots; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);  // leader: 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[i], 2 * kPairEpiWarps);  // leader: the epilogue warps of both CTAs
     }
     for (int i = 0; i < kUnitRing; ++i) {
       mbar_init(&ufull[i], 1);
-      mbar_init(&uempty[i], 10);  // leader: MMA + 4 epilogue warps, peer: producer + 4 epilogue warps
+      mbar_init(&uempty[i], 2 + 2 * kPairEpiWarps);  // leader: MMA + epilogue warps, peer: producer + epilogue warps
     }
     fence_mbar_init();
   }
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
         if (U.phase == 1) {
           const int* done = p.counters + 1 + U.seg;
           Watchdog wd;
-          while (ld_acquire_gpu(done) < 4 * p.tiles1) {
+          while (ld_acquire_gpu(done) < kPairEpiWarps * p.tiles1) {
             __nanosleep(100);
             wd.tick(2);
           }
@@ -607,7 +611,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
     }
   } else if (warp >= 4) {
     // -------------------------------------------------- epilogue (both CTAs)
-    const int q = warp - 4;  // TMEM lane quarter (warp_id % 4)
+    const int q = (warp - 4) & 3;  // TMEM lane quarter (warp_id % 4)
+    const int half = (warp - 4) >> 2;  // which half of the token columns
     int slot = 0, acc = 0;
     uint32_t uphase = 0, aphase = 0;
     while (true) {
@@ -633,7 +638,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_pair_kernel(const __grid_c
         const int tile = 2 * (MT * U.mt + m) + static_cast<int>(rank);
         const uint32_t tb = tmem_base + static_cast<uint32_t>(acc * width) + (static_cast<uint32_t>(q * 32) << 16);
         const bool real = tile < (U.phase == 0 ? p.tiles1 : p.tiles2);  // tiles past the end are padding
-        epilogue_store(p, U, tile, real, q, lane, tb);
+        const int hc = U.nmma >> 1;  // nmma is a multiple of 32: halves of 16-column steps
+        epilogue_store(p, U, tile, real, q, lane, tb, half * hc, (half + 1) * hc);
         published += real ? 1 : 0;
         tc_fence_before();
         __syncwarp();
@@ -677,7 +683,7 @@ static cudaError_t launch_ffn_pair_t(const FfnParams& p, int sm_count, cudaStrea
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sm_count & ~1);
-  cfg.blockDim = dim3(kFfnThreads);
+  cfg.blockDim = dim3(kPairThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
