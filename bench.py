@@ -588,6 +588,10 @@ def run_ep_p2p(args, c, rank, world, local_rank, peers):
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
     hid = [torch.randn((Tl, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(n)]
     outs = [torch.empty_like(h) for h in hid]
+    # every rank's layers are built before any rank waits on a peer's flags
+    # (the peer waits have a watchdog)
+    torch.cuda.synchronize()
+    dist.barrier()
     for i in range(max(args.warmup, n)):
         layers[i % n](hid[i % n], outs[i % n])
     torch.cuda.synchronize()
