@@ -59,16 +59,22 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False, src_d
     os.makedirs(LIB_DIR, exist_ok=True)
     cc = nvcc()
     headers = [os.path.join(csrc, h) for h in HEADERS] + [os.path.join(inc, "lynx_b200.h")]
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         path = os.path.join(csrc, src)
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _newer(obj, [path] + headers):
-            cmd = [cc, *ARCH, *FLAGS, *extra, "-I", inc, "-c", path, "-o", obj]
-            if verbose:
-                print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append([cc, *ARCH, *FLAGS, *extra, "-I", inc, "-c", path, "-o", obj])
+    # translation units compile in parallel (one nvcc each)
+    procs = []
+    for cmd in cmds:
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, pr in procs if pr.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or _newer(lib_path, objs):
         tmp = lib_path + ".tmp"
         cmd = [cc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-cudart", "static"]
