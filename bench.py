@@ -135,11 +135,13 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(cfg_name):
+    """ncu DRAM bytes of ONE launch of this config's FFN kernel (profiles/ffn_traffic.json, written by
+    scripts/summarize_round.py from the round's --set full captures); None when the config was not captured."""
     path = os.path.join(ROOT, "profiles", "ffn_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f)
+            return json.load(f).get(cfg_name)
     return None
 
 
@@ -404,7 +406,7 @@ def run_single(args, c):
     step_bytes = ffn_bytes + N * d * 2 + 2 * T * d * 2
     peak, peak_src = measured_peaks()
     achieved = ffn_bytes / (kern["ffn"] * 1e-3) / 1e9
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.config)
     result = {
         "metric": METRIC, "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,

@@ -108,12 +108,21 @@ def main():
                 "= the L2 -> SM bytes (weights + activation tiles)",
         "kernels": kernels}
     json.dump(summary, open(os.path.join(PROF, f"{tag}_ncu_full_summary.json"), "w"), indent=1)
-    ffn = next(k for k in kernels if "ffn_kernel" in k["Kernel Name"] and "C2" in k["capture"])
-    rd, wr = to_bytes(ffn["dram__bytes_read.sum"]), to_bytes(ffn["dram__bytes_write.sum"])
-    json.dump({"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
-               "source": f"ncu --set full, profiles/{tag}_ncu_full_summary.json (ffn_kernel, C2 Lynx drop 4, "
-                         "4 used experts)", "algorithmic_bytes_per_launch": 4 * 3 * 4096 * 14336 * 2},
-              open(os.path.join(PROF, "ffn_traffic.json"), "w"), indent=1)
+    # per-config K3 traffic: bench.py reports the capture of ITS config's FFN kernel
+    traffic = {}
+    for cfg, tag_cap, used, d, ff in (("c2", "C2", 4, 4096, 14336), ("c5", "C5", 4, 6144, 16384),
+                                      ("c4", "C4", None, 2048, 1408)):
+        ffn = next((k for k in kernels if "ffn_" in k["Kernel Name"] and k["capture"].startswith(tag_cap)), None)
+        if ffn is None:
+            continue
+        rd, wr = to_bytes(ffn["dram__bytes_read.sum"]), to_bytes(ffn["dram__bytes_write.sum"])
+        ent = {"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+               "kernel": ffn["Kernel Name"],
+               "source": f"ncu --set full, profiles/{tag}_ncu_full_summary.json ({ffn['capture']})"}
+        if used is not None:
+            ent["algorithmic_bytes_per_launch"] = used * 3 * d * ff * 2
+        traffic[cfg] = ent
+    json.dump(traffic, open(os.path.join(PROF, "ffn_traffic.json"), "w"), indent=1)
     print(json.dumps({k["Kernel Name"][:40]: k["gpu__time_duration.sum"] for k in kernels}, indent=1))
     sass = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "build", "ffn.o")], capture_output=True,
                           text=True).stdout
