@@ -497,3 +497,62 @@ def test_fused_front_edge_shapes_vs_oracle(T):
         f = lambda t: t.float().cpu().numpy()  # noqa: E731
         ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights)
         assert O.norm_rel_err(_np(y), ref) <= TOL, tag
+
+
+@pytest.mark.parametrize("T", [1, 7, 8, 9, 33, 128, 255, 256])
+def test_wide_router_edge_shapes_vs_oracle(T):
+    """Wide routers (8 < N <= 64: K1's thread-per-token path up to 16, K0's
+    cluster routing + K1's group path above) at the decode batch edges: one
+    token, partial / whole / just over one 4-token routing cluster, 256
+    tokens; N across the 8-expert CTA widths (9, 16, 17, 40, 64), k up to 8,
+    shared experts 0..2; latency policies with drops past the
+    floor, min_experts and rank weights, accuracy policies (top1 / margin),
+    prefill.  Selection bit-exact vs the oracle on the kernel's logits,
+    layer output within the bf16 tolerance."""
+    rng = np.random.default_rng(1000 + T)
+    for rep in range(5):
+        N = int(rng.choice([9, 16, 17, 40, 64]))
+        k = int(rng.integers(1, min(8, N) + 1))
+        S = int(rng.integers(0, 3))
+        d, ff = int(rng.choice([64, 128])), int(rng.choice([64, 192]))
+        decode = rep != 4
+        kind = rep % 3
+        if kind == 0:
+            cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 2)))
+            opol = O.Policy(mode="latency", drop_count=cfg.drop_count)
+        elif kind == 1:
+            mk = int(rng.integers(k, N + 1))
+            rw = tuple(float(x) for x in rng.uniform(0.1, 1.0, size=k))
+            cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 1)), min_experts=mk,
+                                 vote_rank_weights=rw)
+            opol = O.Policy(mode="latency", drop_count=cfg.drop_count, min_experts=mk, vote_rank_weights=rw)
+        else:
+            cfg = L.PolicyConfig(mode="accuracy", confidence_threshold=float(rng.choice([0.1, 0.3])),
+                                 sample_threshold=int(rng.integers(1, 10)), freq_keep_budget=int(rng.integers(1, N + 1)),
+                                 confidence_metric=str(rng.choice(["top1", "margin"])))
+            opol = O.Policy(mode="accuracy", confidence_threshold=cfg.confidence_threshold,
+                            sample_threshold=cfg.sample_threshold, freq_keep_budget=cfg.freq_keep_budget,
+                            confidence_metric=cfg.confidence_metric)
+        model = L.build_swiglu_model(L.MoEModelSpec(1, N, k, d, ff, num_shared_experts=S), seed=T * 10 + rep)
+        g = torch.Generator(device="cuda").manual_seed(rep)
+        hidden = torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16)
+        layer = L.LynxMoELayer(model, 0, T, policy=cfg, phase=L.Phase.DECODE if decode else L.Phase.PREFILL)
+        y = layer(hidden)
+        torch.cuda.synchronize()
+        logits = _np(L.router_logits(model, 0, hidden))
+        ids, probs, full = O.route(logits, k)
+        ref_mask = O.apply(ids, probs, full, opol, decode=decode)
+        tag = dict(T=T, N=N, k=k, S=S, rep=rep, decode=decode, cfg=cfg)
+        assert np.array_equal(_np(layer.expert_ids), ids), tag
+        assert np.allclose(_np(layer.full_probs), full, rtol=1e-12, atol=1e-15), tag
+        assert np.array_equal(_np(layer.assigned), ref_mask.assigned), tag
+        keep = np.zeros(N, dtype=np.uint8)
+        keep[ref_mask.retained] = 1
+        assert np.array_equal(_np(layer.retained_mask), keep), tag
+        assert np.allclose(_np(layer.weights), ref_mask.weights, rtol=1e-12, atol=1e-15), tag
+        assert bool(int(layer.flags.item()) & 1) == bool(ref_mask.clipped), tag
+        w1, w3 = L.unpack_w13(model.w13[0], ff)
+        f = lambda t: t.float().cpu().numpy()  # noqa: E731
+        ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights,
+                               shared=range(N, N + S))
+        assert O.norm_rel_err(_np(y), ref) <= TOL, tag
