@@ -20,7 +20,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "lts__t_sectors_srcunit_tex_op_read.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
            "launch__shared_mem_per_block", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
-           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+           "lts__t_bytes.sum"]
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -64,6 +65,11 @@ def ncu_raw(rep):
             if m in h:
                 i = h.index(m)
                 d[m] = f"{r[i]} {units[i]}".strip()
+        # the top warp-stall reasons (warps stalled per issued instruction)
+        st = [(n.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
+               float(r[i] or 0)) for i, n in enumerate(h)
+              if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")]
+        d["top_stalls_per_issue"] = {n: round(v, 2) for n, v in sorted(st, key=lambda x: -x[1])[:6]}
         out.append(d)
     return out
 
@@ -77,8 +83,8 @@ CAPTURES = [  # (report in gpurun_out/, what it holds)
     ("ffn_full.ncu-rep", "C2 (Mixtral-8x7B layer, T=32, latency drop 4): ffn_kernel"),
     ("ffn_pair_full.ncu-rep", "C5 (Mixtral-8x22B layer, T=256, latency drop 4): ffn_pair_kernel (MT=2)"),
     ("small_full.ncu-rep", "C2: fused front_kernel (K0+K1+K2) and combine_kernel (K4)"),
-    ("r02_ffn_c4.ncu-rep", "C4 (DeepSeek-MoE-16B, T=128, accuracy budget 16): ffn_kernel"),
-    ("r02_k01_c4.ncu-rep", "C4: router_route_kernel (K0 + routing) and route_select_group (K1)"),
+    ("ffn_c4_full.ncu-rep", "C4 (DeepSeek-MoE-16B, T=128, accuracy budget 16): ffn_kernel"),
+    ("k01_c4_full.ncu-rep", "C4: router_route_kernel (K0 + routing) and route_select_group (K1)"),
 ]
 
 
@@ -102,7 +108,7 @@ def main():
                 kernels.append(k)
     summary = {
         "what": "ncu --set full --clock-control none captures, round " + tag[1:],
-        "commands": ["scripts/ncu_round.sh", "scripts/ncu_r02.sh (C4 captures)"],
+        "commands": ["scripts/ncu_round.sh"],
         "note": "per-kernel times are cold-cache serialised replays; dram__bytes_read vs the algorithmic "
                 "used-expert bytes shows each used expert streamed once; lts__t_sectors_srcunit_tex_op_read x 32 B "
                 "= the L2 -> SM bytes (weights + activation tiles)",
