@@ -51,9 +51,14 @@ cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
 // accumulation order (simulator.py:101-112) with a fixed split-K order, so
 // the layer output is bit-reproducible.  One CTA per (token, 512 columns);
 // the token's rows are staged once, then all k*S float4 loads issue together.
+// SPLIT = the split-K slot count when it is 1 or 2 (every BASELINE shape),
+// 0 = any: with a compile-time count the k x SPLIT loads are straight-line
+// (no per-entry index arithmetic) and all issue before the first use.
+template <int SPLIT>
 __global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ CombineArgs a) {
-  __shared__ int s_rows[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
-  __shared__ float s_w[LYNX_MAX_TOPK + LYNX_MAX_SHARED];
+  constexpr int kMaxEntries = LYNX_MAX_TOPK + LYNX_MAX_SHARED;
+  __shared__ int s_rows[kMaxEntries];
+  __shared__ float s_w[kMaxEntries];
   griddep_launch_dependents();
   warm_params(a);
   griddep_wait();  // partial slots come from K3
@@ -73,37 +78,52 @@ __global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ Co
     const float2 h0 = __bfloat1622float2(h[0]), h1 = __bfloat1622float2(h[1]);
     acc = make_float4(h0.x, h0.y, h1.x, h1.y);
   }
-  const int n = a.k * a.split2;
-  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int i0 = 0; i0 < n; i0 += 16) {
-    float4 v[16];
+  auto slot = [&](int s, int row) {
+    return *reinterpret_cast<const float4*>(a.partial + s * a.slot_stride + static_cast<size_t>(row) * a.d + c);
+  };
+  if (SPLIT > 0) {
+    constexpr int S = SPLIT > 0 ? SPLIT : 1;
+    float4 v[kMaxEntries][S];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = min(i0 + u, n - 1);
-      const int j = i / a.split2, s = i - j * a.split2;
-      const int row = max(s_rows[j], 0);
-      v[u] = *reinterpret_cast<const float4*>(a.partial + s * a.slot_stride + static_cast<size_t>(row) * a.d + c);
-    }
+    for (int j = 0; j < kMaxEntries; ++j)
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u;
-      if (i >= n) break;
-      const int j = i / a.split2, s = i - j * a.split2;
-      if (s == 0) {
-        y = v[u];
-      } else {
-        y.x += v[u].x;
-        y.y += v[u].y;
-        y.z += v[u].z;
-        y.w += v[u].w;
-      }
-      if (s == a.split2 - 1 && s_rows[j] >= 0) {
+      for (int s = 0; s < S; ++s)
+        if (j < a.k && s_rows[j] >= 0) v[j][s] = slot(s, s_rows[j]);
+#pragma unroll
+    for (int j = 0; j < kMaxEntries; ++j) {
+      if (j < a.k && s_rows[j] >= 0) {
+        float4 y = v[j][0];
+#pragma unroll
+        for (int s = 1; s < S; ++s) {
+          y.x += v[j][s].x;
+          y.y += v[j][s].y;
+          y.z += v[j][s].z;
+          y.w += v[j][s].w;
+        }
         const float w = s_w[j];
         acc.x += w * y.x;
         acc.y += w * y.y;
         acc.z += w * y.z;
         acc.w += w * y.w;
       }
+    }
+  } else {
+    for (int j = 0; j < a.k; ++j) {
+      const int row = s_rows[j];
+      if (row < 0) continue;
+      float4 y = slot(0, row);
+      for (int s = 1; s < a.split2; ++s) {
+        const float4 u = slot(s, row);
+        y.x += u.x;
+        y.y += u.y;
+        y.z += u.z;
+        y.w += u.w;
+      }
+      const float w = s_w[j];
+      acc.x += w * y.x;
+      acc.y += w * y.y;
+      acc.z += w * y.z;
+      acc.w += w * y.w;
     }
   }
   const size_t o = static_cast<size_t>(t) * a.d + c;
@@ -127,7 +147,10 @@ __global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ Co
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t s) {
-  return launch_pdl(combine_kernel, dim3((a.d + 511) / 512, a.T), dim3(128), 0, s, a);
+  const dim3 grid((a.d + 511) / 512, a.T);
+  if (a.split2 == 1) return launch_pdl(combine_kernel<1>, grid, dim3(128), 0, s, a);
+  if (a.split2 == 2) return launch_pdl(combine_kernel<2>, grid, dim3(128), 0, s, a);
+  return launch_pdl(combine_kernel<0>, grid, dim3(128), 0, s, a);
 }
 
 // ------------------------------------------------------------ trace ring
