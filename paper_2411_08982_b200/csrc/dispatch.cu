@@ -55,7 +55,7 @@ cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
 // 0 = any: with a compile-time count the k x SPLIT loads are straight-line
 // (no per-entry index arithmetic) and all issue before the first use.
 template <int SPLIT>
-__global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ CombineArgs a) {
+__global__ void __launch_bounds__(128, SPLIT == 1 ? 6 : 10) combine_kernel(const __grid_constant__ CombineArgs a) {
   constexpr int kMaxEntries = LYNX_MAX_TOPK + LYNX_MAX_SHARED;
   __shared__ int s_rows[kMaxEntries];
   __shared__ float s_w[kMaxEntries];
@@ -82,29 +82,38 @@ __global__ void __launch_bounds__(128) combine_kernel(const __grid_constant__ Co
     return *reinterpret_cast<const float4*>(a.partial + s * a.slot_stride + static_cast<size_t>(row) * a.d + c);
   };
   if (SPLIT > 0) {
+    // entries in groups whose loads issue together, with registers low enough
+    // for high occupancy (the slots come from HBM: occupancy is the MLP)
     constexpr int S = SPLIT > 0 ? SPLIT : 1;
-    float4 v[kMaxEntries][S];
+    // one split slot: every entry's load in flight at once (C4: 8 rows);
+    // two: four entries (eight loads) per group, registers for 10 CTAs per SM
+    constexpr int G = S == 1 ? kMaxEntries : 4;
+#pragma unroll 1
+    for (int j0 = 0; j0 < a.k; j0 += G) {
+      float4 v[G][S];
 #pragma unroll
-    for (int j = 0; j < kMaxEntries; ++j)
+      for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int s = 0; s < S; ++s)
-        if (j < a.k && s_rows[j] >= 0) v[j][s] = slot(s, s_rows[j]);
+        for (int s = 0; s < S; ++s)
+          if (j0 + g < a.k && s_rows[j0 + g] >= 0) v[g][s] = slot(s, s_rows[j0 + g]);
 #pragma unroll
-    for (int j = 0; j < kMaxEntries; ++j) {
-      if (j < a.k && s_rows[j] >= 0) {
-        float4 y = v[j][0];
+      for (int g = 0; g < G; ++g) {
+        const int j = j0 + g;
+        if (j < a.k && s_rows[j] >= 0) {
+          float4 y = v[g][0];
 #pragma unroll
-        for (int s = 1; s < S; ++s) {
-          y.x += v[j][s].x;
-          y.y += v[j][s].y;
-          y.z += v[j][s].z;
-          y.w += v[j][s].w;
+          for (int s = 1; s < S; ++s) {
+            y.x += v[g][s].x;
+            y.y += v[g][s].y;
+            y.z += v[g][s].z;
+            y.w += v[g][s].w;
+          }
+          const float w = s_w[j];
+          acc.x += w * y.x;
+          acc.y += w * y.y;
+          acc.z += w * y.z;
+          acc.w += w * y.w;
         }
-        const float w = s_w[j];
-        acc.x += w * y.x;
-        acc.y += w * y.y;
-        acc.z += w * y.z;
-        acc.w += w * y.w;
       }
     }
   } else {
