@@ -16,8 +16,10 @@
 // sits at cache positions pos .. pos+Tn-1; `pos` is read from device memory
 // so one captured decode step can be replayed step after step
 // (lynx_advance_position bumps it inside the graph).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lynx_internal.cuh"
 
@@ -64,6 +66,7 @@ constexpr int kQkvPerCta = kAttnThreads / 32;
 constexpr int kOutCols = kAttnThreads * 4;
 constexpr int kChunkFloats = 4096;  // K (or V) floats per chunk: chunk = 4096 / dh positions
 constexpr int kWoPrefetch = 16;     // Wo head rows held in registers from the start
+constexpr int kMaxAttnCluster = 8;  // decode kernel: CTAs (1024-column chunks) per row cluster, d <= 8192
 
 // sum of squares of the whole row (the decode step's input normalisation)
 __device__ __forceinline__ float row_sumsq(const uint16_t* row, int d, float* red) {
@@ -80,16 +83,12 @@ __device__ __forceinline__ float row_sumsq(const uint16_t* row, int d, float* re
   return block_sum(ss, red);
 }
 
-__global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_constant__ AttnArgs a) {
-  griddep_launch_dependents();
-  warm_params(a);
-  griddep_wait();
-  const int row = blockIdx.x;  // b * Tn + i
-  const int b = row / a.Tn, i = row - b * a.Tn;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nout = 3 * a.dh, nvec = a.d >> 3;
-  const int o = blockIdx.y * kQkvPerCta + warp;
-  if (o >= nout) return;
+// Output o of the 3*dh q/k/v projections for token row `row`, one warp:
+// the lane streams its 1/32 of the row and of the weight row together, so
+// the RMSNorm statistic and the dot come out of one pass.  Every lane
+// returns the value.
+__device__ __forceinline__ float qkv_dot(const AttnArgs& a, int row, int o, int lane) {
+  const int nvec = a.d >> 3;
   const uint4* hr = reinterpret_cast<const uint4*>(a.h_in + static_cast<size_t>(row) * a.d);
   const uint4* wr = reinterpret_cast<const uint4*>(a.wqkv + static_cast<size_t>(o) * a.d);
   float ss = 0.f, acc = 0.f;
@@ -110,12 +109,25 @@ __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_con
     ss += __shfl_xor_sync(kAll, ss, off);
     acc += __shfl_xor_sync(kAll, acc, off);
   }
+  // x = h * s1 (s1 = 1 unless the input is the step's rms_norm(prev));
+  // the attention's own rms_norm of x has mean square s1^2 * ss / d
+  const float s1 = a.norm_input ? 1.f / sqrtf(ss / a.d + 1e-12f) : 1.f;
+  const float s2 = 1.f / sqrtf(s1 * s1 * ss / a.d + 1e-12f);
+  return acc * s1 * s2;
+}
+
+__global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_constant__ AttnArgs a) {
+  griddep_launch_dependents();
+  warm_params(a);
+  griddep_wait();
+  const int row = blockIdx.x;  // b * Tn + i
+  const int b = row / a.Tn, i = row - b * a.Tn;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nout = 3 * a.dh;
+  const int o = blockIdx.y * kQkvPerCta + warp;
+  if (o >= nout) return;
+  const float val = qkv_dot(a, row, o, lane);
   if (lane == 0) {
-    // x = h * s1 (s1 = 1 unless the input is the step's rms_norm(prev));
-    // the attention's own rms_norm of x has mean square s1^2 * ss / d
-    const float s1 = a.norm_input ? 1.f / sqrtf(ss / a.d + 1e-12f) : 1.f;
-    const float s2 = 1.f / sqrtf(s1 * s1 * ss / a.d + 1e-12f);
-    const float val = acc * s1 * s2;
     const int which = o / a.dh, c = o - which * a.dh;
     if (which == 0) {
       a.q[static_cast<size_t>(row) * a.dh + c] = val;
@@ -131,13 +143,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_qkv_kernel(const __grid_con
 // columns' partial dots and sum of squares; the row's last CTA sums the
 // chunks in chunk order (deterministic) and writes the f64 logits the way
 // K0 does: dot * 1 / sqrt(ss / d + 1e-12).
-__device__ __forceinline__ void fused_router(const AttnArgs& a, int row, const float (&x)[4],
+// kCluster (the decode kernel, one cluster per row): the chunk partials go
+// to the leader CTA's shared memory over DSMEM and the leader finishes, with
+// the same chunk-order sums -- no global partials and no arrival counter.
+template <bool kCluster>
+__device__ __forceinline__ void fused_router(const AttnArgs& a, int row, int chunk, int chunks, const float (&x)[4],
                                              const uint2 (&rw)[LYNX_MAX_FUSED_ROUTER]) {
   __shared__ float red2[kAttnThreads / 32][LYNX_MAX_FUSED_ROUTER + 1];
+  __shared__ float s_chunks[kMaxAttnCluster][LYNX_MAX_FUSED_ROUTER + 1];  // leader: every chunk's partials
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int N = a.N, chunks = gridDim.y, chunk = blockIdx.y;
-  const bool live = blockIdx.y * kOutCols + threadIdx.x * 4 < a.d;
+  const int N = a.N;
+  const bool live = chunk * kOutCols + threadIdx.x * 4 < a.d;
   float v = x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kAll, v, off);
@@ -156,6 +173,26 @@ __device__ __forceinline__ void fused_router(const AttnArgs& a, int row, const f
     if (lane == 0) red2[warp][e] = dot;
   }
   __syncthreads();
+  if (kCluster) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    if (threadIdx.x <= N) {
+      float t = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red2[w][threadIdx.x];
+      cluster.map_shared_rank(&s_chunks[0][0], 0)[chunk * (LYNX_MAX_FUSED_ROUTER + 1) + threadIdx.x] = t;
+    }
+    cluster.sync();
+    if (chunk == 0 && threadIdx.x < N) {
+      float dot = 0.f, ss = 0.f;
+      for (int c = 0; c < chunks; ++c) {
+        dot += s_chunks[c][threadIdx.x];
+        ss += s_chunks[c][N];
+      }
+      const double inv = 1.0 / sqrt(static_cast<double>(ss) / a.d + 1e-12);
+      a.logits[static_cast<size_t>(row) * N + threadIdx.x] = static_cast<double>(dot) * inv;
+    }
+    return;
+  }
   float* part = a.rpart + (static_cast<size_t>(row) * chunks + chunk) * (N + 1);
   if (threadIdx.x <= N) {
     float t = 0.f;
@@ -183,6 +220,17 @@ __device__ __forceinline__ void fused_router(const AttnArgs& a, int row, const f
   }
 }
 
+// kCluster = false: attn_out, grid (rows, column chunks), after attn_qkv.
+// kCluster = true: the decode step (Tn = 1) in ONE kernel, grid (column
+// chunks, rows) with one thread-block cluster per row: the cluster's CTAs
+// first split the row's 3*dh q/k/v projections (qkv_dot, as attn_qkv), send q
+// to every CTA's shared memory over DSMEM and write k/v to the cache; after
+// a cluster barrier (release/acquire: the new cache entries are visible to
+// the cluster) each CTA runs attn_out's attention and its 1024 output
+// columns, and the fused router finishes in the leader over DSMEM.  The
+// same arithmetic as attn_qkv + attn_out, so the same bits; it saves a
+// launch boundary and the router's global partials / arrival counter.
+template <bool kCluster>
 __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ float sm[];  // K chunk | V chunk | scores chunk | ctx partials
   __shared__ float red[32];
@@ -190,8 +238,11 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   __shared__ float ctx[LYNX_MAX_DHEAD];
   griddep_launch_dependents();
   warm_params(a);
+  // DSMEM rule: peers may store into this CTA's qs only once it runs
+  if (kCluster) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   griddep_wait();
-  const int row = blockIdx.x;
+  const int row = kCluster ? blockIdx.y : blockIdx.x;
+  const int ochunk = kCluster ? blockIdx.x : blockIdx.y, nochunk = kCluster ? gridDim.x : gridDim.y;
   const int b = row / a.Tn, i = row - b * a.Tn;
   const int dh = a.dh, chunk = kChunkFloats / dh;
   float* Ks = sm;
@@ -199,7 +250,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   float* sc = Vs + kChunkFloats;
   float* part = sc + chunk;  // [blockDim/dh][dh]
   // ---- everything this CTA reads, issued up front
-  const int col = blockIdx.y * kOutCols + threadIdx.x * 4;
+  const int col = ochunk * kOutCols + threadIdx.x * 4;
   const bool live = col < a.d;
   const uint16_t* hrow = a.h_in + static_cast<size_t>(row) * a.d;
   uint2 hres = make_uint2(0, 0);
@@ -216,7 +267,26 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
         if (e < a.N) rw[e] = __ldg(reinterpret_cast<const uint2*>(a.router_wt + static_cast<size_t>(e) * a.d + col));
     }
   }
-  if (threadIdx.x < dh) qs[threadIdx.x] = a.q[static_cast<size_t>(row) * dh + threadIdx.x];
+  if (kCluster) {
+    // q / k / v: output o = ochunk + nochunk * (warp + 8 r) on this CTA
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    for (int o = ochunk + nochunk * warp; o < 3 * dh; o += nochunk * (kAttnThreads / 32)) {
+      const float val = qkv_dot(a, row, o, lane);
+      const int which = o / dh, c = o - which * dh;
+      if (which == 0) {
+        if (lane < nochunk) cluster.map_shared_rank(&qs[0], lane)[c] = val;
+      } else if (lane == 0) {
+        float* cache = which == 1 ? a.kcache : a.vcache;
+        cache[(static_cast<size_t>(b) * a.max_len + *a.pos + i) * dh + c] = val;
+      }
+    }
+    cluster.sync();  // q in every CTA, the new k / v entries visible to the cluster
+  } else if (threadIdx.x < dh) {
+    qs[threadIdx.x] = a.q[static_cast<size_t>(row) * dh + threadIdx.x];
+  }
   const int total = *a.pos + i + 1;  // causal: cache positions 0 .. pos+i
   const float* K = a.kcache + static_cast<size_t>(b) * a.max_len * dh;
   const float* V = a.vcache + static_cast<size_t>(b) * a.max_len * dh;
@@ -309,7 +379,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
       rout[3] = y1.y;
     }
   }
-  if (a.router_wt) fused_router(a, row, rout, rw);
+  if (a.router_wt) fused_router<kCluster>(a, row, ochunk, nochunk, rout, rw);
 }
 
 __global__ void advance_position_kernel(int32_t* pos, int by) {
@@ -323,6 +393,16 @@ size_t attn_out_smem(int d, int dh, int max_len) {
   return sizeof(float) * (2 * kChunkFloats + kChunkFloats / dh + (kAttnThreads / dh) * dh);
 }
 
+// LYNX_ATTN_CLUSTER=0 keeps the two-kernel decode attention (A/B switch).
+static bool decode_cluster_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LYNX_ATTN_CLUSTER");
+    v = (e && e[0] == '0' && !e[1]) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
   const size_t smem_a = 0;
   const size_t smem_b = attn_out_smem(a.d, a.dh, a.max_len);
@@ -330,18 +410,37 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured != dev) {
-    cudaError_t e = cudaFuncSetAttribute(attn_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(attn_out_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_out_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(attn_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     configured = dev;
   }
-  const int rows = a.B * a.Tn;
+  const int rows = a.B * a.Tn, chunks = (a.d + kOutCols - 1) / kOutCols;
+  if (a.Tn == 1 && chunks <= kMaxAttnCluster && decode_cluster_enabled()) {
+    // decode: one kernel, a cluster of `chunks` CTAs per row
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(chunks, rows);
+    cfg.blockDim = dim3(kAttnThreads);
+    cfg.dynamicSmemBytes = smem_b;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = chunks;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, attn_out_kernel<true>, a);
+  }
   cudaError_t e = launch_pdl(attn_qkv_kernel, dim3(rows, (3 * a.dh + kQkvPerCta - 1) / kQkvPerCta),
                              dim3(kAttnThreads), smem_a, s, a);
   if (e != cudaSuccess) return e;
-  return launch_pdl(attn_out_kernel, dim3(rows, (a.d + kOutCols - 1) / kOutCols), dim3(kAttnThreads), smem_b, s,
-                    a);
+  return launch_pdl(attn_out_kernel<false>, dim3(rows, chunks), dim3(kAttnThreads), smem_b, s, a);
 }
 
 cudaError_t launch_advance_position(int32_t* pos, int by, cudaStream_t s) {
