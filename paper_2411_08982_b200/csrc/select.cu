@@ -1672,16 +1672,18 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
   const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
   if (run_policy && !accuracy && a.pol.n_rank_weights == 0 && T * k <= 256) {
-    // latency_policy with unit votes on warp 0 alone (policy.py:116-148,
-    // 232-264): ballots count each expert's slots, lane e ranks expert e by
-    // (count desc, index asc) against the others, the first N - eff are kept.
-    // Integer arithmetic: the same decisions as batch_policy, no block barrier.
+    // latency_policy with unit votes on warp 0 (policy.py:116-148, 232-264):
+    // the ids are staged by the whole CTA in one load round, then ballots
+    // count each expert's slots, lane e ranks expert e by (count desc, index
+    // asc) against the others, the first N - eff are kept.  Integer
+    // arithmetic: the same decisions as batch_policy.
+    for (int i = tid; i < T * k; i += blockDim.x) IDS[i] = a.ids[i];
+    __syncthreads();
     if (tid < 32) {
       int cnt = 0;
       for (int i0 = 0; i0 < T * k; i0 += 32) {
         const int i = i0 + tid;
-        const int id = i < T * k ? a.ids[i] : -1;
-        if (i < T * k) IDS[i] = id;
+        const int id = i < T * k ? IDS[i] : -1;
         for (int e = 0; e < N; ++e) {
           const unsigned m = __ballot_sync(kFull, id == e);
           if (tid == e) cnt += __popc(m);
@@ -1953,6 +1955,15 @@ cudaError_t launch_front(const SelectArgs& a, const uint16_t* hidden, const uint
   f.logits_in = logits_in;
   const size_t smem = front_smem_bytes(a.T, a.N, a.k, d);
   if (smem > 48 * 1024) return cudaErrorInvalidValue;
+  static int configured = -1;  // static + dynamic shared memory may pass 48 KB: opt in once per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(front_kernel<8>),
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = dev;
+  }
   return launch_pdl(front_kernel<8>, dim3(a.T), dim3(256), smem, s, f);
 }
 
@@ -2013,13 +2024,13 @@ cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
     const int threads = ((a.T > a.N ? a.T : a.N) + 31) / 32 * 32;
     static int configured8 = -1, configured16 = -1;
     if (a.N <= 8) {
-      if (smem > 48 * 1024) {
+      {  // static + dynamic shared memory may pass 48 KB: opt in (once per device)
         cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_fast<8>), configured8);
         if (e != cudaSuccess) return e;
       }
       return launch_pdl(route_select_fast<8>, dim3(1), dim3(threads), smem, s, a);
     }
-    if (smem > 48 * 1024) {
+    {
       cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(route_select_fast<16>), configured16);
       if (e != cudaSuccess) return e;
     }
@@ -2040,7 +2051,7 @@ cudaError_t launch_route_select(const SelectArgs& a, cudaStream_t s) {
                : reinterpret_cast<const void*>(route_select_group<8, false>);
     conf = &configured[given ? 3 : 2];
   }
-  if (smem > 48 * 1024) {
+  {  // the kernel's static shared memory (policy / plan tables) adds to `smem`
     cudaError_t e = allow_big_smem(fn, *conf);
     if (e != cudaSuccess) return e;
   }
@@ -2056,7 +2067,7 @@ cudaError_t launch_plan(const int32_t* asg, const double* w, int T, int N, int k
   const size_t smem = static_cast<size_t>(N) * W * 8;
   if (smem > kSelectMaxSmem) return cudaErrorInvalidValue;
   static int configured = -1;
-  if (smem > 48 * 1024) {
+  {
     cudaError_t e = allow_big_smem(reinterpret_cast<const void*>(plan_kernel), configured);
     if (e != cudaSuccess) return e;
   }
