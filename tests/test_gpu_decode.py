@@ -228,3 +228,19 @@ def test_decode_stack_vs_reference_simulate():
             m, rm = masks[(ev["event"], ev["layer"])], ev["mask"]
             assert list(m.retained) == list(rm["retained"]) and m.clipped == rm["clipped"], ev
             assert m.num_tokens == rm["num_tokens"] and m.num_important == rm["num_important"], ev
+
+
+def test_decode_stack_two_kernel_attention():
+    """Decode steps normally run the attention as one clustered kernel
+    (attn_out_kernel<true>); LYNX_ATTN_CLUSTER=0 keeps attn_qkv + attn_out.
+    Rerun the stack's parity tests through the two-kernel path."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LYNX_ATTN_CLUSTER="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_decode.py"), "-k",
+                        "teacher_forced or reference_simulate or graph_replay"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])

@@ -423,6 +423,23 @@ def test_cta_pair_kernel_forced_on_every_shape():
         assert r.returncode == 0, (force, r.stdout[-3000:], r.stderr[-2000:])
 
 
+@pytest.mark.parametrize("kb2_per", ["3", "1000"])
+def test_split_k_slot_counts(kb2_per):
+    """K4 is specialised on the split-K slot count (1 or 2 at every BASELINE
+    shape, a generic loop otherwise): force many slots (LYNX_KB2_PER=3, the
+    generic path) and a single slot (1000) and rerun the layer parity tests."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LYNX_KB2_PER=kb2_per)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_ffn.py"), "-k",
+                        "random_layer or shared_experts or deepseek or swiglu_vs_oracle or tanh2"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (kb2_per, r.stdout[-3000:], r.stderr[-2000:])
+
+
 @pytest.mark.parametrize("case", ["c2", "acc", "t256", "n5"])
 def test_fused_front_identical_to_kernel_chain(case, tmp_path):
     """The fused front (K0 + K1 + K2 in one launch, N <= 8) against the
