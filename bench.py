@@ -433,7 +433,10 @@ def run_single(args, c):
                 "api": "paper_2411_08982_b200.LynxMoELayer.stream_host (per-step H2D + lynx_moe_layer graph + D2H, "
                        "copies overlapped with neighbouring steps)",
                 "single_step_host_api_ms": ms_host_step},
-        "gpu_launches": 5 * args.steps,
+        # kernels per layer step: the fused front (N <= 8, T <= 256, no shared experts) + K3 + K4,
+        # else K0 + K1 + K2 + K3 + K4
+        "gpu_launches": (3 if (N <= 8 and T <= 256 and not c.get("S", 0)
+                               and os.environ.get("LYNX_FUSED_FRONT") != "0") else 5) * args.steps,
         "clocks": clocks.summary(),
     }
     return result
@@ -515,7 +518,10 @@ def run_stack(args, c):
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": B * d * 2, "d2h_bytes_per_step": B * d * 2,
                 "api": "paper_2411_08982_b200.DecodeStack.step (one CUDA graph per step)"},
-        "gpu_launches": (nl * (6 if head.fused_router else 7) + 1) * args.steps,
+        # per layer: the decode attention (one clustered kernel for d <= 8192, else attn_qkv + attn_out),
+        # the fused front, K3, K4; per step: the position advance
+        "gpu_launches": (nl * ((1 if d <= 8192 and os.environ.get("LYNX_ATTN_CLUSTER") != "0" else 2) + 3) + 1)
+                        * args.steps,
         "clocks": clocks,
     }
 
