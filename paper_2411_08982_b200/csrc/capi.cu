@@ -95,6 +95,17 @@ bool fused_front_enabled() {
   return v == 1;
 }
 
+// LYNX_L2_DISCARD=0 keeps K3's dead scratch in L2 (written back when evicted); 2 / 3 drop only
+// the split-K slots / only H and the gathered rows (A/B switch).
+int l2_discard_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LYNX_L2_DISCARD");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 // LYNX_ROUTE_IN_K1=1 keeps the routing in K1 for N > 16 (A/B switch).
 bool route_in_k0_enabled() {
   static int v = -1;
@@ -349,6 +360,21 @@ int gather_and_ffn(const lynx_layer_t* L, const uint16_t* hidden, int T, uint16_
   ca.tok_weight = o.tok_weight;
   ca.out_bf16 = out_bf16;
   ca.out_f32 = out_f32;
+  // Dropping K3's dead scratch from L2 (instead of writing it back while the
+  // next layer streams) pays where the scratch is large next to K4's own
+  // work: the wide-d_ff layers whose down projection K4 sums from two split-K
+  // slots (C2 -1.6 us, C5 T=256 -16 us); at C4 (one slot, 8 rows per token)
+  // the discards lengthen K4 more than they save (+1 us).  LYNX_L2_DISCARD:
+  // 0 off, 1 on (default, this rule), 2 slots only, 3 scratch only.
+  const int dmode = g.split2 >= 2 ? l2_discard_mode() : 0;
+  if (dmode == 1 || dmode == 3) {
+    ca.discard_rows = o.n_rows;
+    ca.discard_base[0] = reinterpret_cast<uint8_t*>(fp.h);
+    ca.discard_row_bytes[0] = sizeof(uint16_t) * static_cast<size_t>(ff);
+    ca.discard_base[1] = reinterpret_cast<uint8_t*>(ga.x_perm);
+    ca.discard_row_bytes[1] = sizeof(uint16_t) * static_cast<size_t>(d);
+  }
+  if (dmode == 1 || dmode == 2) ca.discard_partials = d % 32 == 0 ? 1 : 0;
   record(ev, 2, s);
   return cuda_status(launch_combine(ca, s));
 }

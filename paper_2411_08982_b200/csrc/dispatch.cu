@@ -135,6 +135,20 @@ __global__ void __launch_bounds__(128, SPLIT == 1 ? 6 : 10) combine_kernel(const
       acc.w += w * y.w;
     }
   }
+  if (a.discard_partials) {
+    // this warp's 8-thread groups have consumed their 128-byte lines of every
+    // slot row: drop them from L2 unwritten (K4 is their only reader)
+    __syncwarp();
+    if (live && (threadIdx.x & 7) == 0)
+      for (int j = 0; j < a.k; ++j) {
+        const int row = s_rows[j];
+        if (row < 0) continue;
+        for (int s2 = 0; s2 < a.split2; ++s2)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.partial + s2 * a.slot_stride +
+                                                             static_cast<size_t>(row) * a.d + c)
+                       : "memory");
+      }
+  }
   const size_t o = static_cast<size_t>(t) * a.d + c;
   if (a.peer_mode) {
     // the token's owner gathers every rank's partial in slot [rank]
@@ -145,13 +159,23 @@ __global__ void __launch_bounds__(128, SPLIT == 1 ? 6 : 10) combine_kernel(const
       if (threadIdx.x == 0) signal_peers(a.peers, kSigBack, *a.peers.epoch + 1);
     }
   } else if (!live) {
-    return;
   } else if (a.out_f32) {
     *reinterpret_cast<float4*>(a.out_f32 + o) = acc;
   } else {
     __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(a.out_bf16 + o);
     out[0] = __floats2bfloat162_rn(acc.x, acc.y);
     out[1] = __floats2bfloat162_rn(acc.z, acc.w);
+  }
+  if (a.discard_rows) {
+    // K3 is complete: the H rows and gathered token rows it used are dead --
+    // drop them from L2 unwritten (the plan's row count, not the capacity)
+    const size_t rows = static_cast<size_t>(*a.discard_rows);
+    const size_t nthr = static_cast<size_t>(gridDim.x) * gridDim.y * blockDim.x;
+    const size_t me = (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      for (size_t i = me; i < rows * a.discard_row_bytes[r] / 128; i += nthr)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.discard_base[r] + i * 128) : "memory");
   }
 }
 

@@ -138,6 +138,14 @@ struct CombineArgs {
   const float* tok_weight;
   uint16_t* out_bf16;  // exactly one of the outputs is set
   float* out_f32;
+  // K3's scratch, dead once K3 completes (H, the gathered token rows):
+  // dropped from L2 without write-back (discard.global.L2), and the split-K
+  // slots after K4 reads them (discard_partials; needs d % 32 == 0 so no
+  // 128-byte line spans two rows)
+  const int32_t* discard_rows;  // rows of both regions in use (the plan's n_rows), or null: no discard
+  uint8_t* discard_base[2];
+  size_t discard_row_bytes[2];
+  int discard_partials;
 };
 
 struct GatherArgs {
