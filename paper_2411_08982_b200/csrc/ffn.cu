@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) ffn_pair_kernel(const __grid_
       Unit U;
       if (!decode_unit_pair(p, nseg, u, tp1, tp2, U)) break;
       int published = 0;
+      LYNX_TRACE_T0;
 #pragma unroll 1
       for (int m = 0; m < MT; ++m) {
         mbar_wait(&tfull[acc], (aphase >> acc) & 1u, 8);
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) ffn_pair_kernel(const __grid_
         __syncwarp();
         if (lane == 0) red_release_gpu_add(p.counters + 1 + U.seg, published);
       }
+      if (threadIdx.x == 128) LYNX_TRACE_REC(4, u);  // unit drained (trace build: per-CTA unit timeline)
     }
   }
   tc_fence_before();

@@ -30,6 +30,9 @@ def main():
     if "--c4" in sys.argv:
         T, N, k, d, ff, S = 128, 64, 6, 2048, 1408, 2
         pol = L.PolicyConfig(mode="accuracy", freq_keep_budget=16)
+    elif "--c5" in sys.argv:  # CTA-pair kernel: role-4 records are unit drains (epilogue end), per CTA
+        T, N, k, d, ff, S = 256, 8, 2, 6144, 16384, 0
+        pol = L.PolicyConfig(mode="latency", drop_count=4)
     else:
         T, N, k, d, ff, S = 32, 8, 2, 4096, 14336, 0
         pol = L.PolicyConfig(mode="latency", drop_count=4)
@@ -57,7 +60,7 @@ def main():
     # unit classes (queue order: phase-0 units, then phase-1 units)
     tiles1 = 2 * ((ff + 63) // 64) * 64 // 128
     ngather = 0
-    nA = used * tiles1
+    nA = used * (tiles1 // 4 if "--c5" in sys.argv else tiles1)  # pair kernel, MT=2: 4 tiles per unit
     out = {"records": int(n), "kernel_span_us": float((t1.max() - base) / 1e3), "nA": nA}
     m = role == 4
     dur = (t1[m] - t0[m]) / 1e3
