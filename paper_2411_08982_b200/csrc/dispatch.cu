@@ -61,13 +61,14 @@ __global__ void __launch_bounds__(128, SPLIT == 1 ? 6 : 10) combine_kernel(const
   __shared__ float s_w[kMaxEntries];
   griddep_launch_dependents();
   warm_params(a);
-  griddep_wait();  // partial slots come from K3
+  // K3 releases this launch only after its own wait: the plan (token rows,
+  // weights) and the residual are complete, so they load before our wait --
+  // only the split-K slots need K3 to have finished
   const int t = blockIdx.y;
   if (threadIdx.x < a.k) {
     s_rows[threadIdx.x] = a.tok_rows[t * a.k + threadIdx.x];
     s_w[threadIdx.x] = a.tok_weight[t * a.k + threadIdx.x];
   }
-  __syncthreads();
   const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const bool live = c0 < a.d;
   const int c = live ? c0 : 0;
@@ -78,6 +79,8 @@ __global__ void __launch_bounds__(128, SPLIT == 1 ? 6 : 10) combine_kernel(const
     const float2 h0 = __bfloat1622float2(h[0]), h1 = __bfloat1622float2(h[1]);
     acc = make_float4(h0.x, h0.y, h1.x, h1.y);
   }
+  __syncthreads();
+  griddep_wait();  // partial slots come from K3
   auto slot = [&](int s, int row) {
     return *reinterpret_cast<const float4*>(a.partial + s * a.slot_stride + static_cast<size_t>(row) * a.d + c);
   };

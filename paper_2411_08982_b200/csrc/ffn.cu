@@ -196,10 +196,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kUnitRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Let K4 (combine) launch now: its CTAs are small enough to sit beside this
-  // one and wait in griddepcontrol.wait, so its launch latency leaves the
-  // critical path (K4 still reads nothing before this grid completes).
-  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
@@ -229,6 +225,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
   // Everything above overlapped the previous kernel (programmatic launch);
   // the dispatch plan and gathered rows are only read after this point.
   griddep_wait();
+  // Let K4 (combine) launch now: its CTAs are small enough to sit beside this
+  // one and wait in griddepcontrol.wait, so its launch latency leaves the
+  // critical path.  Released only after our own wait, so K4 starts after the
+  // plan's writer completed and may read the plan (token rows, weights)
+  // before its own wait; the split-K slots it reads only after this grid.
+  griddep_launch_dependents();
 #ifdef LYNX_TRACE
   const uint64_t cta_t0 = globaltimer();
 #endif
@@ -455,7 +457,6 @@ __global__ void __launch_bounds__(kPairThreads, 1) ffn_pair_kernel(const __grid_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) ffn_pair_kernel(const __grid_
   cluster_sync();  // both CTAs' barriers initialised and TMEM allocated
   tc_fence_after();
   griddep_wait();
+  griddep_launch_dependents();  // K4 may launch now (see ffn_kernel)
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *p.n_seg;
   const int tp1 = (p.tiles1 + 2 * MT - 1) / (2 * MT), tp2 = (p.tiles2 + 2 * MT - 1) / (2 * MT);
