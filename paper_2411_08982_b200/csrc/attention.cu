@@ -22,10 +22,23 @@
 #include <stdlib.h>
 
 #include "lynx_internal.cuh"
+#include "ptx.cuh"
 
 namespace lynx {
 
 constexpr int kAttnThreads = 256;
+
+// Diagnostic library only (-DLYNX_TRACE): phase timestamps of the decode
+// attention kernel (CTA (0, 0)), read back by lynx_debug_attn_ts().
+#ifdef LYNX_TRACE
+__device__ unsigned long long g_attn_ts[16];
+#define ATT_TS(i)                                                                             \
+  do {                                                                                        \
+    if (kCluster && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_attn_ts[i] = globaltimer(); \
+  } while (0)
+#else
+#define ATT_TS(i) (void)0
+#endif
 constexpr unsigned kAll = 0xffffffffu;
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -240,7 +253,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   warm_params(a);
   // DSMEM rule: peers may store into this CTA's qs only once it runs
   if (kCluster) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  ATT_TS(0);
   griddep_wait();
+  ATT_TS(1);
   const int row = kCluster ? blockIdx.y : blockIdx.x;
   const int ochunk = kCluster ? blockIdx.x : blockIdx.y, nochunk = kCluster ? gridDim.x : gridDim.y;
   const int b = row / a.Tn, i = row - b * a.Tn;
@@ -283,7 +298,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
         cache[(static_cast<size_t>(b) * a.max_len + *a.pos + i) * dh + c] = val;
       }
     }
+    ATT_TS(2);
     cluster.sync();  // q in every CTA, the new k / v entries visible to the cluster
+    ATT_TS(3);
   } else if (threadIdx.x < dh) {
     qs[threadIdx.x] = a.q[static_cast<size_t>(row) * dh + threadIdx.x];
   }
@@ -291,6 +308,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   const float* K = a.kcache + static_cast<size_t>(b) * a.max_len * dh;
   const float* V = a.vcache + static_cast<size_t>(b) * a.max_len * dh;
   const float s1 = a.norm_input ? 1.f / sqrtf(row_sumsq(hrow, a.d, red) / a.d + 1e-12f) : 1.f;
+  ATT_TS(4);
   const float inv_sqrt = 1.f / sqrtf(static_cast<float>(dh));
   const int per = blockDim.x / dh;
   float m_run = -INFINITY, l_run = 0.f, c_run = 0.f;  // c_run: this thread's (c, slice) ctx partial
@@ -332,6 +350,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
     }
     __syncthreads();  // Ks/Vs/sc reused by the next chunk
   }
+  ATT_TS(5);
   if (threadIdx.x < per * dh) part[(threadIdx.x / dh) * dh + threadIdx.x % dh] = c_run;
   __syncthreads();
   if (threadIdx.x < dh) {
@@ -340,6 +359,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
     ctx[threadIdx.x] = acc / l_run;
   }
   __syncthreads();
+  ATT_TS(6);
   float rout[4] = {0.f, 0.f, 0.f, 0.f};
   if (live) {
     float o[4] = {0.f, 0.f, 0.f, 0.f};
@@ -379,7 +399,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
       rout[3] = y1.y;
     }
   }
+  ATT_TS(7);
   if (a.router_wt) fused_router<kCluster>(a, row, ochunk, nochunk, rout, rw);
+  ATT_TS(8);
 }
 
 __global__ void advance_position_kernel(int32_t* pos, int by) {
@@ -442,6 +464,12 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   return launch_pdl(attn_out_kernel<false>, dim3(rows, chunks), dim3(kAttnThreads), smem_b, s, a);
 }
+
+#ifdef LYNX_TRACE
+extern "C" int lynx_debug_attn_ts(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_attn_ts, sizeof(g_attn_ts)) == cudaSuccess ? 16 : -1;
+}
+#endif
 
 cudaError_t launch_advance_position(int32_t* pos, int by, cudaStream_t s) {
   return launch_pdl(advance_position_kernel, dim3(1), dim3(32), 0, s, pos, by);
