@@ -100,14 +100,16 @@ __device__ __forceinline__ float row_sumsq(const uint16_t* row, int d, float* re
 // the lane streams its 1/32 of the row and of the weight row together, so
 // the RMSNorm statistic and the dot come out of one pass.  Every lane
 // returns the value.
-__device__ __forceinline__ float qkv_dot(const AttnArgs& a, int row, int o, int lane) {
+// hs (optional): the row staged in shared memory by the caller, so the warp's
+// loads in flight are its weight row's only (same arithmetic, same bits).
+__device__ __forceinline__ float qkv_dot(const AttnArgs& a, int row, int o, int lane, const uint4* hs = nullptr) {
   const int nvec = a.d >> 3;
   const uint4* hr = reinterpret_cast<const uint4*>(a.h_in + static_cast<size_t>(row) * a.d);
   const uint4* wr = reinterpret_cast<const uint4*>(a.wqkv + static_cast<size_t>(o) * a.d);
   float ss = 0.f, acc = 0.f;
 #pragma unroll 16
   for (int v = lane; v < nvec; v += 32) {
-    const uint4 hu = __ldg(hr + v), wu = __ldg(wr + v);
+    const uint4 hu = hs ? hs[v] : __ldg(hr + v), wu = __ldg(wr + v);
     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hu);
     const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wu);
 #pragma unroll
@@ -271,33 +273,48 @@ __global__ void __launch_bounds__(kAttnThreads) attn_out_kernel(const __grid_con
   uint2 hres = make_uint2(0, 0);
   uint2 wo[kWoPrefetch];  // the first kWoPrefetch head rows of Wo (all of them at the reference's dh = 16)
   uint2 rw[LYNX_MAX_FUSED_ROUTER];  // fused router: this thread's 4 columns of every expert's router row
-  if (live) {
-    hres = __ldg(reinterpret_cast<const uint2*>(hrow + col));
+  auto prefetch = [&]() {
+    if (live) {
+      hres = __ldg(reinterpret_cast<const uint2*>(hrow + col));
 #pragma unroll
-    for (int c = 0; c < kWoPrefetch; ++c)
-      if (c < dh) wo[c] = __ldg(reinterpret_cast<const uint2*>(a.wo + static_cast<size_t>(c) * a.d + col));
-    if (a.router_wt) {
+      for (int c = 0; c < kWoPrefetch; ++c)
+        if (c < dh) wo[c] = __ldg(reinterpret_cast<const uint2*>(a.wo + static_cast<size_t>(c) * a.d + col));
+      if (a.router_wt) {
 #pragma unroll
-      for (int e = 0; e < LYNX_MAX_FUSED_ROUTER; ++e)
-        if (e < a.N) rw[e] = __ldg(reinterpret_cast<const uint2*>(a.router_wt + static_cast<size_t>(e) * a.d + col));
+        for (int e = 0; e < LYNX_MAX_FUSED_ROUTER; ++e)
+          if (e < a.N) rw[e] = __ldg(reinterpret_cast<const uint2*>(a.router_wt + static_cast<size_t>(e) * a.d + col));
+      }
     }
-  }
+  };
+  // decode kernel: the projections' loads go first, the output-side
+  // prefetch after them (it has the attention's duration to land)
+  if (!kCluster) prefetch();
   if (kCluster) {
-    // q / k / v: output o = ochunk + nochunk * (warp + 8 r) on this CTA
+    // q / k / v: output o = ochunk + nochunk * (warp + 8 r) on this CTA; the
+    // row is staged in shared memory once, so each warp's loads in flight
+    // are only its weight row's (one round trip per projection)
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
+    __shared__ uint4 s_row[8192 / 8];  // d <= 8192 (kMaxAttnCluster chunks of 1024)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int v = threadIdx.x; v < (a.d >> 3); v += blockDim.x) s_row[v] = __ldg(reinterpret_cast<const uint4*>(hrow) + v);
+    const int pos = *a.pos;  // loaded once: a store address must not stall the next projection's loads
+    __syncthreads();
+    ATT_TS(10);
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    ATT_TS(11);
     for (int o = ochunk + nochunk * warp; o < 3 * dh; o += nochunk * (kAttnThreads / 32)) {
-      const float val = qkv_dot(a, row, o, lane);
+      const float val = qkv_dot(a, row, o, lane, s_row);
       const int which = o / dh, c = o - which * dh;
       if (which == 0) {
         if (lane < nochunk) cluster.map_shared_rank(&qs[0], lane)[c] = val;
       } else if (lane == 0) {
         float* cache = which == 1 ? a.kcache : a.vcache;
-        cache[(static_cast<size_t>(b) * a.max_len + *a.pos + i) * dh + c] = val;
+        cache[(static_cast<size_t>(b) * a.max_len + pos + i) * dh + c] = val;
       }
+      if (o == ochunk) ATT_TS(9);  // warp 0's first projection done
     }
+    prefetch();
     ATT_TS(2);
     cluster.sync();  // q in every CTA, the new k / v entries visible to the cluster
     ATT_TS(3);

@@ -23,14 +23,17 @@ def main():
     attn = L.build_attention(nl, d, 16, seed=1)
     stack = L.DecodeStack(model, attn, B, max_len=64, policy=L.PolicyConfig(mode="latency", drop_count=4))
     stack.prefill(torch.randn((B, 16, d)).to(torch.bfloat16))
-    rows = []
+    rows, qk = [], []
     for _ in range(8):
         stack.step()
         torch.cuda.synchronize()
         buf = np.zeros(16, dtype=np.uint64)
         lib.lynx_debug_attn_ts(buf.ctypes.data)
         rows.append(np.diff(buf[:9].astype(np.int64)) / 1e3)
+        qk.append(np.diff(buf[[1, 10, 11, 9, 2]].astype(np.int64)) / 1e3)
     m = np.median(np.array(rows[2:]), axis=0)
+    print("qkv split (us): stage row, cluster wait, first projection, rest:",
+          np.round(np.median(np.array(qk[2:]), axis=0), 2).tolist())
     for n, v in zip(NAMES, m):
         print(f"{n:28s} {v:7.2f} us")
     print(f"{'total after wait':28s} {m[1:].sum():7.2f} us")
