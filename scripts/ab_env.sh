@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of an env switch on one box: ab_env2.sh VAR "cfgs" -> bench + timeline for VAR=1 / VAR=0, twice
+# A/B of an env switch on one box: ab_env.sh VAR "cfgs" -> bench + timeline for VAR=1 / VAR=0, twice
 cd "$(dirname "$0")/.."
 var=$1; cfgs=$2
 for c in $cfgs; do

@@ -373,6 +373,64 @@ def test_random_layer_configs_vs_oracle(seed):
     assert O.norm_rel_err(_np(y), ref) <= TOL, tag
 
 
+@pytest.mark.parametrize("seed", range(32))
+def test_random_layer_configs_large_batches_vs_oracle(seed):
+    """A second randomised sweep for the large-batch paths: T 257..2048 (K1
+    in global memory once its per-token arrays do not fit shared memory,
+    expert segments split at 256 rows, the CTA-pair K3 on wide segments),
+    rank-weighted latency votes and min_experts floors included."""
+    rng = np.random.default_rng(5000 + seed)
+    N = int(rng.choice([2, 8, 9, 16, 17, 40, 64]))
+    k = int(rng.integers(1, min(8, N) + 1))
+    S = int(rng.choice([0, 0, 1, 2]))
+    T = int(rng.choice([257, 333, 512, 700, 1024, 2048]))
+    d = int(rng.choice([64, 136, 256]))
+    ff = int(rng.choice([64, 120, 192]))
+    decode = bool(rng.integers(0, 4))
+    kind = int(rng.integers(0, 3))
+    if kind == 0:
+        cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 1)))
+        opol = O.Policy(mode="latency", drop_count=cfg.drop_count)
+    elif kind == 1:
+        mk = int(rng.integers(k, N + 1))
+        rw = tuple(float(x) for x in rng.uniform(0.1, 1.0, size=k))
+        cfg = L.PolicyConfig(mode="latency", drop_count=int(rng.integers(0, N + 1)), min_experts=mk,
+                             vote_rank_weights=rw)
+        opol = O.Policy(mode="latency", drop_count=cfg.drop_count, min_experts=mk, vote_rank_weights=rw)
+    else:
+        mk = int(rng.integers(k, N + 1)) if rng.integers(0, 2) else None
+        cfg = L.PolicyConfig(mode="accuracy", confidence_threshold=float(rng.choice([0.1, 0.3, 0.5])),
+                             sample_threshold=int(rng.integers(1, 40)), min_experts=mk,
+                             freq_keep_budget=int(rng.integers(1, N + 1)),
+                             confidence_metric=str(rng.choice(["top1", "margin"])))
+        opol = O.Policy(mode="accuracy", confidence_threshold=cfg.confidence_threshold,
+                        sample_threshold=cfg.sample_threshold, min_experts=mk,
+                        freq_keep_budget=cfg.freq_keep_budget, confidence_metric=cfg.confidence_metric)
+    spec = L.MoEModelSpec(1, N, k, d, ff, num_shared_experts=S)
+    model = L.build_swiglu_model(spec, seed=seed + 100)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    hidden = torch.randn((T, d), generator=g, device="cuda").to(torch.bfloat16)
+    layer = L.LynxMoELayer(model, 0, T, policy=cfg, phase=L.Phase.DECODE if decode else L.Phase.PREFILL)
+    y = layer(hidden)
+    torch.cuda.synchronize()
+    logits = _np(L.router_logits(model, 0, hidden))
+    ids, probs, full = O.route(logits, k)
+    ref_mask = O.apply(ids, probs, full, opol, decode=decode)
+    tag = dict(N=N, k=k, S=S, T=T, d=d, ff=ff, decode=decode, cfg=cfg)
+    assert np.array_equal(_np(layer.expert_ids), ids), tag
+    assert np.array_equal(_np(layer.assigned), ref_mask.assigned), tag
+    keep = np.zeros(N, dtype=np.uint8)
+    keep[ref_mask.retained] = 1
+    assert np.array_equal(_np(layer.retained_mask), keep), tag
+    assert np.allclose(_np(layer.weights), ref_mask.weights, rtol=1e-12, atol=1e-15), tag
+    assert bool(int(layer.flags.item()) & 1) == bool(ref_mask.clipped), tag
+    w1, w3 = L.unpack_w13(model.w13[0], ff)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    ref = O.forward_swiglu(f(hidden), f(w1), f(w3), f(model.w2[0]), ref_mask.assigned, ref_mask.weights,
+                           round_h_bf16=True, shared=range(N, N + S))
+    assert O.norm_rel_err(_np(y), ref) <= TOL, tag
+
+
 @pytest.mark.parametrize("T,N,k,S,mode", [(4096, 64, 8, 2, "accuracy"), (4096, 64, 8, 0, "latency"),
                                           (4096, 8, 2, 0, "latency"), (1024, 33, 5, 1, "accuracy")])
 def test_layer_at_maximum_sizes_vs_oracle(T, N, k, S, mode):
