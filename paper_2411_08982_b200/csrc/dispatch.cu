@@ -50,7 +50,7 @@ cudaError_t launch_gather(const GatherArgs& a, int sm_count, cudaStream_t s) {
 // j over the token's experts ascending and s in order: the reference's
 // accumulation order (simulator.py:101-112) with a fixed split-K order, so
 // the layer output is bit-reproducible.  One CTA per (token, 512 columns);
-// the token's rows are staged once, then all k*S float4 loads issue together.
+// the token's rows are staged once, then the slot loads issue in groups.
 // SPLIT = the split-K slot count when it is 1 or 2 (every BASELINE shape),
 // 0 = any: with a compile-time count the k x SPLIT loads are straight-line
 // (no per-entry index arithmetic) and all issue before the first use.
