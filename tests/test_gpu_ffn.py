@@ -481,6 +481,22 @@ def test_cta_pair_kernel_forced_on_every_shape():
         assert r.returncode == 0, (force, r.stdout[-3000:], r.stderr[-2000:])
 
 
+@pytest.mark.parametrize("env", ["LYNX_ROUTE_IN_K1=1", "LYNX_FFN_MT=1", "LYNX_L2_DISCARD=0", "LYNX_L2_DISCARD=2"])
+def test_runtime_switches_keep_parity(env):
+    """The A/B switches (run-time switches) change how the layer
+    runs, never its results: rerun the layer parity tests under each."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    key, val = env.split("=")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_ffn.py"), "-k",
+                        "random_layer_configs_vs or deepseek or swiglu_vs_oracle or tanh2"],
+                       env=dict(os.environ, **{key: val}), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (env, r.stdout[-3000:], r.stderr[-2000:])
+
+
 @pytest.mark.parametrize("kb2_per", ["3", "1000"])
 def test_split_k_slot_counts(kb2_per):
     """K4 is specialised on the split-K slot count (1 or 2 at every BASELINE
