@@ -1536,10 +1536,12 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
 // Grid-wide barrier of the fused front (all CTAs resident, see above):
 // arrivals count up with acquire-release atomics, the last arriver resets
 // the count and publishes the next generation with a release store.
-__device__ __forceinline__ void grid_barrier(int* sync, int nblocks) {
+// `gen` is the generation word as it stood when the kernel started (read by
+// thread 0 early, off the barrier's critical path: only this launch's
+// barrier changes it, and the launch that wrote it last has completed).
+__device__ __forceinline__ void grid_barrier(int* sync, int nblocks, int gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int gen = *reinterpret_cast<volatile int*>(sync + 1);  // read before arriving
     if (atom_add_acq_rel_gpu(sync, 1) == nblocks - 1) {
       *reinterpret_cast<volatile int*>(sync) = 0;
       st_release_gpu(sync + 1, gen + 1);
@@ -1583,6 +1585,9 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
     s_flags = 0;
   }
   warm_params(f);
+  // the barrier generation: last written by the previous front on this
+  // workspace, which completed before this launch's predecessor started
+  const int gen0 = tid == 0 ? *reinterpret_cast<volatile int*>(f.sync + 1) : 0;
   griddep_wait();  // hidden comes from the previous kernel
   FRONT_TS(0);
 
@@ -1653,7 +1658,7 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
     }
   }
   FRONT_TS(2);
-  grid_barrier(f.sync, T);
+  grid_barrier(f.sync, T, gen0);
   griddep_launch_dependents();  // every CTA is resident: the expert FFN may launch now
   FRONT_TS(3);
 
