@@ -547,6 +547,34 @@ def _ep_stats(used_local, world, c, ms, phase_ms, phase_names):
     }
 
 
+def _ep_parity(c, rank, world, Tl, pol, out_local):
+    """The EP step against the single-device layer on the same global batch:
+    layer copy 0 (seed 100) rebuilt whole on every rank, every rank's first
+    input regenerated from its seed; this rank's rows of the reference vs its
+    EP output, norm-wise max |y - y_ref| / max |y_ref|, max over ranks.  The
+    EP sum runs in rank order, the single-device combine in expert order: the
+    same experts, another association, so a tolerance (1e-2), not equality."""
+    import torch
+
+    import paper_2411_08982_b200 as L
+    d, ff, N, k = c["d"], c["ff"], c["N"], c["k"]
+    spec = L.MoEModelSpec(num_layers=1, num_experts=N, top_k=k, d_model=d, d_ff=ff)
+    full = L.build_swiglu_model(spec, seed=100)
+    xs = []
+    for r in range(world):
+        g = torch.Generator(device="cuda").manual_seed(1000 + r)
+        xs.append(torch.randn((Tl, d), generator=g, device="cuda").to(torch.bfloat16))
+    ref = L.LynxMoELayer(full, 0, Tl * world, policy=pol)(torch.cat(xs))[rank * Tl:(rank + 1) * Tl].float()
+    torch.cuda.synchronize()
+    err = float((out_local.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+    del full, ref, xs
+    torch.cuda.empty_cache()
+    err = _max_over_ranks(err)
+    if not err <= 1e-2:
+        raise RuntimeError(f"EP output differs from the single-device layer: max rel err {err:.3e}")
+    return err
+
+
 def _ep_result(args, c, world, Tl, ms, ms_e2e, stats, transport, kernel_note, launches, clocks):
     peak, peak_src = measured_peaks()
     crit = stats["critical_path_bytes"]
@@ -664,6 +692,8 @@ def run_ep_p2p(args, c, rank, world, local_rank, peers):
     torch.cuda.synchronize()
     ms_e2e = _max_over_ranks(c0.elapsed_time(c1) / steps)
     args.steps = steps
+    layers[0](hid[0], outs[0])
+    stats["parity_max_rel_err_vs_single_device"] = _ep_parity(c, rank, world, Tl, pol, outs[0])
     return _ep_result(args, c, world, Tl, ms, ms_e2e, stats,
                       "nvlink peer memory (lynx_ep_p2p_*, CUDA-IPC shared buffers; stores issued by K0 / the "
                       "dispatch kernel / K4, release-acquire flags)",
@@ -752,6 +782,8 @@ def run_ep(args, c, rank, world, local_rank):
     c1.record()
     torch.cuda.synchronize()
     ms_e2e = _max_over_ranks(c0.elapsed_time(c1) / args.steps)
+    stats["parity_max_rel_err_vs_single_device"] = _ep_parity(c, rank, world, Tl, pol,
+                                                              EP.ep_layer(shape, ops[0], hid[0]))
     return _ep_result(args, c, world, Tl, ms, ms_e2e, stats, "NCCL all_gather + all_to_all_single (torch.distributed)",
                       "ffn_kernel per rank (critical path)", 6, clocks)
 

@@ -41,7 +41,8 @@ def line_map(obj, fn):
 def main():
     rep, fn, obj = sys.argv[1:4]
     top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    kfilt = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]] if "--kernel" in sys.argv else []
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", *kfilt],
                          capture_output=True, text=True).stdout.split("\n")
     rows = list(csv.reader(out[1:]))
     hdr = rows[0]

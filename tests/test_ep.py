@@ -232,7 +232,7 @@ def test_bench_multi_rank_path_runs(config, transport, batch):
     local ranks (here all on GPU 0: --share-gpu, gloo), runs the EP step at
     the config's fixed global batch (C5: decode batch 256 = 64 rows per rank)
     and prints one JSON line with the per-rank / critical-path / aggregate
-    bytes.  Per-rank statistics differ between ranks, so every collective
+    bytes and the EP output's error against the single-device layer.  Per-rank statistics differ between ranks, so every collective
     must use one dtype on all ranks."""
     import json
     import subprocess
@@ -254,5 +254,7 @@ def test_bench_multi_rank_path_runs(config, transport, batch):
     assert run["critical_path_bytes"] == max(run["expert_bytes_per_rank"])
     assert abs(run["aggregate_bytes"] - sum(run["expert_bytes_per_rank"])) < 1
     assert ("nccl" in run["transport"].lower()) == (transport == "nccl")
+    # the EP output against the single-device layer on the same global batch (bench checks it too)
+    assert run["parity_max_rel_err_vs_single_device"] <= 1e-2
     if transport == "nccl":
         assert 0 <= run["comm_share"] <= 1
