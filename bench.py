@@ -369,6 +369,23 @@ def run_single(args, c):
             for j, nm in enumerate(names)}
     step_b = statistics.mean(evs[i][0].elapsed_time(evs[i][5]) for i in range(kp))
 
+    # (B2) this GPU's achievable READ bandwidth, measured live (a read-only
+    # reduction over 4 GiB, best of 5): the expert stream only reads, and a
+    # read can beat MEASURED_PEAKS.json's copy figure (read + write)
+    xbuf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda").view(torch.int64)
+    xbuf.fill_(1)
+    best_rd = 1e9
+    for _ in range(5):
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        torch.amax(xbuf)
+        r1.record()
+        torch.cuda.synchronize()
+        best_rd = min(best_rd, r0.elapsed_time(r1))
+    read_peak = (4 << 30) / (best_rd * 1e-3) / 1e9
+    del xbuf
+    torch.cuda.empty_cache()
+
     # (C) end to end through the public API with pinned host buffers: every
     # step copies its own input host->device and its output device->host.
     # LynxMoELayer.stream_host overlaps those PCIe copies with the
@@ -422,6 +439,8 @@ def run_single(args, c):
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src,
                      "frac_of_8TBs": achieved / 8000.0,
+                     "read_peak_gbs": read_peak, "frac_of_read_peak": achieved / read_peak,
+                     "read_peak_source": "measured live in this run: torch.amax over 4 GiB (read-only), best of 5",
                      "algorithmic_bytes_per_launch": ffn_bytes,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                      "traffic_source": traffic.get("source") if traffic else None,
