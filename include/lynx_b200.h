@@ -198,9 +198,10 @@ int lynx_moe_forward_partial(const lynx_layer_t *layer, const uint16_t *hidden, 
  * _apply_routing + forward_layer (simulator.py:245-266, 86-113).
  * `sel` may be NULL; when given, the selection/mask outputs are copied out.
  * For N <= 8, T <= LYNX_SEG_ROWS and no shared experts, K0..K2 run as one
- * fused launch synchronised by two grid barriers whose words live in the
+ * fused launch synchronised by a grid barrier whose words live in the
  * workspace: zero-fill the workspace once before its first use (every call
- * leaves those words zero again; a workspace serves calls in stream order). */
+ * leaves those words ready for the next; a workspace serves calls in stream
+ * order). */
 int lynx_moe_layer(const lynx_layer_t *layer, const uint16_t *hidden, int T, int decode,
                    const lynx_policy_t *policy, uint16_t *out, const lynx_selection_t *sel,
                    void *workspace, size_t workspace_bytes, lynx_stream_t stream);

@@ -1507,7 +1507,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
 // Results are identical to router_logits_kernel + route_select_fast +
 // plan_dispatch + gather_kernel (same arithmetic, same order).  The barrier
 // words (f.sync) must be zero before the first launch; every launch leaves
-// them zero.  Co-residency: the T CTAs only wait for each other (the next
+// them ready for the next one (grid_barrier).  Co-residency: the T CTAs only wait for each other (the next
 // kernel's programmatic launch is released after the barrier), and T <= 256
 // small CTAs always fit the 148 SMs.
 struct FrontArgs {
@@ -1516,39 +1516,51 @@ struct FrontArgs {
   const uint16_t* router_wt;  // [N, d] bf16
   int d;
   uint16_t* x_perm;           // [rows_cap, d] gathered rows
-  int* sync;                  // [4]: barrier arrivals, generation, non-finite flag accumulator (zero)
+  int* sync;                  // [4]: arrival counters (even / odd launches), non-finite flag accumulator,
+                              //   generation (all zero before the first launch)
   const double* logits_in;    // [T, N] given logits (the decode stack's fused router), or null: phase A
 };
 
 #ifdef LYNX_TRACE
+__device__ unsigned long long g_front_cta[4 * 256];  // per CTA: entry, after wait, at the barrier, after it
+#define FRONT_CTA_TS(i)                                                                       \
+  do {                                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x < 256) g_front_cta[4 * blockIdx.x + (i)] = globaltimer(); \
+  } while (0)
 #define FRONT_TS(i)                                                                \
   do {                                                                             \
     if (blockIdx.x == 0 && threadIdx.x == 0) g_sel_ts[24 + (i)] = globaltimer(); \
   } while (0)
 #else
 #define FRONT_TS(i) (void)0
+#define FRONT_CTA_TS(i) (void)0
 #endif
 
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid-wide barrier of the fused front (all CTAs resident, see above):
-// arrivals count up with acquire-release atomics, the last arriver resets
-// the count and publishes the next generation with a release store.
-// `gen` is the generation word as it stood when the kernel started (read by
-// thread 0 early, off the barrier's critical path: only this launch's
-// barrier changes it, and the launch that wrote it last has completed).
-__device__ __forceinline__ void grid_barrier(int* sync, int nblocks, int gen) {
+// Grid-wide barrier of the fused front (all CTAs resident, see above), on
+// two arrival counters used alternately by launch parity (f.sync[0], [1]):
+// each CTA arrives with one release reduction -- no returned value to wait
+// for -- and polls its counter until every CTA has arrived, so the barrier
+// completes one L2 round trip after the last arrival (the last arriver no
+// longer resets a count and publishes a generation first: that cost
+// 1.6-2.2 us from the last arrival to the first exit).  The launch's
+// parity comes from the generation word f.sync[3], read at kernel start
+// (the launch that last wrote it has completed); after its wait CTA 0
+// zeroes the OTHER counter, which only the previous launch used, and
+// after the barrier it advances the generation for the next launch.
+__device__ __forceinline__ void red_release_gpu_add_int(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier(int* counter, int nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (atom_add_acq_rel_gpu(sync, 1) == nblocks - 1) {
-      *reinterpret_cast<volatile int*>(sync) = 0;
-      st_release_gpu(sync + 1, gen + 1);
-    } else {
-      Watchdog wd;
-      while (ld_acquire_gpu(sync + 1) == gen) wd.tick(9);
-    }
+    red_release_gpu_add_int(counter, 1);
+    Watchdog wd;
+    while (ld_acquire_gpu(counter) < nblocks) wd.tick(9);
   }
   __syncthreads();
 }
@@ -1569,6 +1581,7 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   __shared__ int s_rows[LYNX_MAX_TOPK];
   __shared__ int s_nrows;
   extern __shared__ __align__(16) uint8_t s_dyn[];
+  FRONT_CTA_TS(0);
   const int T = a.T, N = a.N, k = a.k, t = blockIdx.x, tid = threadIdx.x;
   const int W = (T + 31) >> 5;
   double* WT = reinterpret_cast<double*>(s_dyn);                            // [T*k] remap weights
@@ -1587,9 +1600,12 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   warm_params(f);
   // the barrier generation: last written by the previous front on this
   // workspace, which completed before this launch's predecessor started
-  const int gen0 = tid == 0 ? *reinterpret_cast<volatile int*>(f.sync + 1) : 0;
+  __shared__ int s_gen;
+  if (tid == 0) s_gen = *reinterpret_cast<volatile int*>(f.sync + 3);
   griddep_wait();  // hidden comes from the previous kernel
+  if (t == 0 && tid == 0) f.sync[1 - (s_gen & 1)] = 0;  // the previous launch's counter, for the next one
   FRONT_TS(0);
+  FRONT_CTA_TS(1);
 
   // token t's hidden row -> shared memory (cp.async), for the gather in E
   const int nvec = f.d >> 3;
@@ -1658,13 +1674,16 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
     }
   }
   FRONT_TS(2);
-  grid_barrier(f.sync, T, gen0);
+  FRONT_CTA_TS(2);
+  grid_barrier(f.sync + (s_gen & 1), T);  // (s_gen: written before the first __syncthreads of the barrier)
+  FRONT_CTA_TS(3);
   griddep_launch_dependents();  // every CTA is resident: the expert FFN may launch now
   FRONT_TS(3);
 
   if (t == 0 && tid == 0) {
     s_flags = f.sync[2];  // every CTA's non-finite report precedes barrier 1
     f.sync[2] = 0;
+    f.sync[3] = s_gen + 1;  // the next launch's parity
   }
 
   // the probability rows of this thread's tokens (remap, D), issued before
@@ -2102,5 +2121,8 @@ cudaError_t launch_vote(const int32_t* ids, int T, int k, int N, const lynx_poli
 #ifdef LYNX_TRACE
 extern "C" int lynx_debug_select_ts(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, lynx::g_sel_ts, sizeof(lynx::g_sel_ts)) == cudaSuccess ? 32 : -1;
+}
+extern "C" int lynx_debug_front_cta_ts(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, lynx::g_front_cta, sizeof(lynx::g_front_cta)) == cudaSuccess ? 1024 : -1;
 }
 #endif

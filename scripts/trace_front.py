@@ -34,6 +34,17 @@ def main():
         ts = buf[24:31].astype(np.int64)
         rows.append(np.diff(ts) / 1e3)
     m = np.median(np.array(rows[2:]), axis=0)
+    if "--c4" not in sys.argv:  # per-CTA skew of the last step (entry, after the wait, at / after the barrier)
+        lib.lynx_debug_front_cta_ts.argtypes = [ctypes.c_void_p]
+        cb = np.zeros(1024, dtype=np.uint64)
+        lib.lynx_debug_front_cta_ts(cb.ctypes.data)
+        c = cb[:4 * T].reshape(T, 4).astype(np.int64)
+        w0 = c[:, 1].min()
+        rel = (c - w0) / 1e3
+        print("per-CTA (us, vs the first wait return): entry min/max", round(rel[:, 0].min(), 2), round(rel[:, 0].max(), 2),
+              "| wait return min/max", round(rel[:, 1].min(), 2), round(rel[:, 1].max(), 2),
+              "| barrier arrival min/median/max", round(rel[:, 2].min(), 2), round(float(np.median(rel[:, 2])), 2),
+              round(rel[:, 2].max(), 2), "| barrier exit min/max", round(rel[:, 3].min(), 2), round(rel[:, 3].max(), 2))
     for n, v in zip(NAMES[1:], m):
         print(f"{n:22s} {v:7.2f} us")
     print(f"{'total after wait':22s} {m.sum():7.2f} us")
