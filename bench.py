@@ -369,23 +369,6 @@ def run_single(args, c):
             for j, nm in enumerate(names)}
     step_b = statistics.mean(evs[i][0].elapsed_time(evs[i][5]) for i in range(kp))
 
-    # (B2) this GPU's achievable READ bandwidth, measured live (a read-only
-    # reduction over 4 GiB, best of 5): the expert stream only reads, and a
-    # read can beat MEASURED_PEAKS.json's copy figure (read + write)
-    xbuf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda").view(torch.int64)
-    xbuf.fill_(1)
-    best_rd = 1e9
-    for _ in range(5):
-        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        r0.record()
-        torch.amax(xbuf)
-        r1.record()
-        torch.cuda.synchronize()
-        best_rd = min(best_rd, r0.elapsed_time(r1))
-    read_peak = (4 << 30) / (best_rd * 1e-3) / 1e9
-    del xbuf
-    torch.cuda.empty_cache()
-
     # (C) end to end through the public API with pinned host buffers: every
     # step copies its own input host->device and its output device->host.
     # LynxMoELayer.stream_host overlaps those PCIe copies with the
@@ -416,6 +399,23 @@ def run_single(args, c):
     s1.record()
     torch.cuda.synchronize()
     ms_host_step = s0.elapsed_time(s1) / 20
+
+    # (D) this GPU's achievable READ bandwidth, measured live (a read-only
+    # reduction over 4 GiB, best of 5): the expert stream only reads, and a
+    # read can beat MEASURED_PEAKS.json's copy figure (read + write)
+    xbuf = torch.empty(4 << 30, dtype=torch.uint8, device="cuda").view(torch.int64)
+    xbuf.fill_(1)
+    best_rd = 1e9
+    for _ in range(5):
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        torch.amax(xbuf)
+        r1.record()
+        torch.cuda.synchronize()
+        best_rd = min(best_rd, r0.elapsed_time(r1))
+    read_peak = (4 << 30) / (best_rd * 1e-3) / 1e9
+    del xbuf
+    torch.cuda.empty_cache()
 
     # algorithmic bytes of one layer step (used experts only) and of one FFN launch
     mean_used = statistics.mean(used[i % n] for i in range(kp))
