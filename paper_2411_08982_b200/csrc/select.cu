@@ -1695,17 +1695,23 @@ __global__ void __launch_bounds__(256) front_kernel(const __grid_constant__ Fron
   // C) batch policy (every CTA, identical)
   const bool run_policy = a.decode && a.pol.mode != LYNX_POLICY_NONE;
   const bool accuracy = run_policy && a.pol.mode == LYNX_POLICY_ACCURACY;
-  if (run_policy && !accuracy && a.pol.n_rank_weights == 0 && T * k <= 256) {
+  if (run_policy && !accuracy && a.pol.n_rank_weights == 0) {
     // latency_policy with unit votes on warp 0 (policy.py:116-148, 232-264):
-    // the ids are staged by the whole CTA in one load round, then ballots
-    // count each expert's slots, lane e ranks expert e by (count desc, index
-    // asc) against the others, the first N - eff are kept.  Integer
+    // the ids are staged by the whole CTA in one load round and counted --
+    // by ballots on warp 0 for up to 256 slots, by shared-memory atomics of
+    // the whole CTA beyond -- then lane e ranks expert e by (count desc,
+    // index asc) against the others, the first N - eff are kept.  Integer
     // arithmetic: the same decisions as batch_policy.
-    for (int i = tid; i < T * k; i += blockDim.x) IDS[i] = a.ids[i];
+    const bool by_atomics = T * k > 256;
+    for (int i = tid; i < T * k; i += blockDim.x) {
+      const int id = a.ids[i];
+      IDS[i] = id;
+      if (by_atomics && id >= 0 && id < N) atomicAdd(&s_icount[id], 1);
+    }
     __syncthreads();
     if (tid < 32) {
-      int cnt = 0;
-      for (int i0 = 0; i0 < T * k; i0 += 32) {
+      int cnt = by_atomics && tid < N ? s_icount[tid] : 0;
+      for (int i0 = 0; i0 < (by_atomics ? 0 : T * k); i0 += 32) {
         const int i = i0 + tid;
         const int id = i < T * k ? IDS[i] : -1;
         for (int e = 0; e < N; ++e) {
