@@ -18,7 +18,7 @@ NAMES = ["entry -> griddep_wait", "qkv (DSMEM q, cache k/v)", "cluster.sync", "r
 def main():
     lib = nat.lib()
     lib.lynx_debug_attn_ts.argtypes = [ctypes.c_void_p]
-    nl, B, d, ff = 2, 64, 4096, 14336
+    nl, B, d, ff = 2, 64, 4096, (64 if "--tiny-experts" in sys.argv else 14336)
     model = L.build_swiglu_model(L.MoEModelSpec(nl, 8, 2, d, ff), seed=0)
     attn = L.build_attention(nl, d, 16, seed=1)
     stack = L.DecodeStack(model, attn, B, max_len=64, policy=L.PolicyConfig(mode="latency", drop_count=4))
