@@ -1507,9 +1507,9 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
 // Results are identical to router_logits_kernel + route_select_fast +
 // plan_dispatch + gather_kernel (same arithmetic, same order).  The barrier
 // words (f.sync) must be zero before the first launch; every launch leaves
-// them ready for the next one (grid_barrier).  Co-residency: the T CTAs only wait for each other (the next
-// kernel's programmatic launch is released after the barrier), and T <= 256
-// small CTAs always fit the 148 SMs.
+// them ready for the next one (grid_barrier).  Co-residency: the T CTAs only
+// wait for each other (the next kernel's programmatic launch is released
+// after the barrier), and T <= 256 small CTAs always fit the 148 SMs.
 struct FrontArgs {
   SelectArgs s;               // selection outputs + plan (s.logits unused)
   const uint16_t* hidden;     // [T, d] bf16
