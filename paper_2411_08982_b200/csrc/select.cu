@@ -1536,10 +1536,6 @@ __device__ unsigned long long g_front_cta[4 * 256];  // per CTA: entry, after wa
 #define FRONT_CTA_TS(i) (void)0
 #endif
 
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // Grid-wide barrier of the fused front (all CTAs resident, see above), on
 // two arrival counters used alternately by launch parity (f.sync[0], [1]):
 // each CTA arrives with one release reduction -- no returned value to wait
