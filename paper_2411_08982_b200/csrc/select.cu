@@ -48,9 +48,15 @@ __device__ unsigned long long g_sel_ts[32];
   do {                                                 \
     if (threadIdx.x == 0) g_sel_ts[i] = globaltimer(); \
   } while (0)
+// K0 (router_route_kernel) phases of block (0, 0), slots 8..12 (free when K1 runs on a given selection)
+#define K0_TS(i)                                                                                   \
+  do {                                                                                             \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_sel_ts[8 + (i)] = globaltimer(); \
+  } while (0)
 #else
 #define SEL_TS(i) (void)0
 #define SEL_TS_LOCAL(i) (void)0
+#define K0_TS(i) (void)0
 #endif
 
 // numpy's pairwise float64 summation (oracle.pairwise_sum): < 8 terms added
@@ -1427,9 +1433,12 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
   const int t0 = blockIdx.y * TPC, c = static_cast<int>(cluster.block_rank());
   const int n0 = c * 8;
   if (c == 0) np_exp_stage(s_exp);  // read by warp 0 after cluster.sync()
+  K0_TS(0);
   griddep_wait();  // hidden may be produced by the previous kernel
+  K0_TS(1);
   double z[TPC];
   router_dots8_multi<TPC>(hidden, wt, t0, T, d, N, n0, z);
+  K0_TS(2);
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (threadIdx.x < 8 && n0 + threadIdx.x < N) {
 #pragma unroll
@@ -1440,6 +1449,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
     }
   }
   cluster.sync();
+  K0_TS(3);
   if (c != 0 || threadIdx.x >= 32) return;
   // warp 0 of the leader: group g = lanes 8g..8g+7 routes token t0 + g; the
   // groups past TPC (or past T) shadow on zeros (shuffles stay warp-converged)
@@ -1484,6 +1494,7 @@ __global__ void __launch_bounds__(256) router_route_kernel(const uint16_t* __res
       probs[t * k + r] = bad ? NAN : bv;
     }
   }
+  K0_TS(4);
 }
 
 // ------------------------------------------- fused front (N <= 8, T <= 256)

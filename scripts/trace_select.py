@@ -52,7 +52,11 @@ def main():
                 sub = buf[[3, 20, 21, 22, 23, 4]].astype(np.int64)
                 print(label, "remap sub-phases (us): start, slot0, slots1.., pre-sum, sum+write:",
                       np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
-            if buf[8]:  # group path sub-phases (warp 0's own timeline)
+            if "--c4" in sys.argv and not warm and buf[12]:  # K0 (router_route_kernel) phases, block (0,0)
+                k0 = buf[8:13].astype(np.int64)
+                print(label, "K0 (us): entry->wait, logits, cluster wait+DSMEM+sync, routing:",
+                      np.round(np.diff(k0) / 1e3, 2).tolist(), file=sys.stderr)
+            if buf[8] and "--c4" not in sys.argv:  # group path sub-phases (warp 0's own timeline)
                 sub = buf[[1, 8, 9, 10, 11, 12, 13]].astype(np.int64)
                 print(label, "route sub-phases (us): load+max, exp, sum, div, write, topk:",
                       np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
