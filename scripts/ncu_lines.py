@@ -44,7 +44,12 @@ def main():
     kfilt = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]] if "--kernel" in sys.argv else []
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", *kfilt],
                          capture_output=True, text=True).stdout.split("\n")
-    rows = list(csv.reader(out[1:]))
+    rows = list(csv.reader(out))
+    # skip "Kernel Name" lines and keep only the first kernel's table
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    end = next((i for i in range(start + 1, len(rows)) if rows[i] and rows[i][0] in ("Kernel Name", "Address")),
+               len(rows))
+    rows = rows[start:end]
     hdr = rows[0]
     data = [r for r in rows[1:] if len(r) == len(hdr)]
     base = int(data[0][0], 16)
