@@ -893,6 +893,16 @@ __device__ __forceinline__ void remap_row(const double* prow, bool live, int t, 
   // in (p desc, c asc) order -- so one arg-max round per displaced slot of
   // the warp's neediest token, not one per slot -- or collapse onto the best
   // retained expert when none is left.
+  // slot r's original expert and full_probs[t, e] (policy.py:206-208) on
+  // lane r: the row's k loads from `full` (global when K0 routed) issue in
+  // one round instead of one dependent round trip per slot
+  if (live)
+    for (int r = j; r < k; r += 8) {
+      const int e = IDS[t * k + r];
+      ASG[t * k + r] = e;
+      WT[t * k + r] = prow[e];
+    }
+  SEL_TS_LOCAL(21);
   uint32_t occ = 0, dmask = 0;  // occ: lane-local compact bits; dmask: displaced slots
 #pragma unroll 1
   for (int r = 0; r < k; ++r) {
@@ -901,13 +911,12 @@ __device__ __forceinline__ void remap_row(const double* prow, bool live, int t, 
       lane_mark(occ, __popcll(keep & ((1ull << e) - 1ull)), j);
     else
       dmask |= 1u << r;
-    if (live && j == 0) {
-      ASG[t * k + r] = e;
-      WT[t * k + r] = prow[e];  // full_probs[t, assigned] (policy.py:206-208)
-    }
   }
+  __syncwarp();  // the displaced slots' picks below overwrite lane r's stores
+  SEL_TS_LOCAL(24);
   const int d = live ? __popc(dmask) : 0;
   const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(d));  // warp-uniform: shuffles stay converged
+  SEL_TS_LOCAL(25);
 #pragma unroll 1
   for (int i = 0; i < rounds; ++i) {
     double bv;

@@ -19,7 +19,7 @@ def main():
     lib = nat.lib()
     lib.lynx_debug_select_ts.argtypes = [ctypes.c_void_p]
     if "--c4" in sys.argv:  # DeepSeek-MoE-16B shape, accuracy policy
-        T, N, k, d, ff, S = 128, 64, 6, 2048, 1408, 2
+        T, N, k, d, ff, S = 128, 64, 6, 2048, (64 if "--tiny-experts" in sys.argv else 1408), 2
         cfg = L.PolicyConfig(mode="accuracy", freq_keep_budget=16)
     else:
         T, N, k, d, ff, S = 32, 8, 2, 4096, 14336, 0
@@ -32,6 +32,13 @@ def main():
     for label, warm in (("cold_after_stream", False), ("warm_repeat", True)):
         rows = []
         for rep in range(5):
+            if "--touch" in sys.argv and not warm:
+                # read the layer's workspace and selection buffers first (L2 and TLB warm for
+                # K1's data; its code stays cold): separates data from instruction-fetch cost
+                lay = layers[rep % 2]
+                for b in (lay.workspace, lay.expert_ids, lay.probs, lay.full_probs, lay.conf, lay.counts,
+                          lay.retained_mask, lay.assigned, lay.weights, lay.important):
+                    b.view(torch.uint8).sum()
             layers[rep % 2](h)  # streams weights -> evicts L2
             torch.cuda.synchronize()
             if warm:
@@ -49,8 +56,9 @@ def main():
                 print(label, "policy sub-phases (us): important, sample-rank, votes, order, keep:",
                       np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
             if buf[20]:  # group remap sub-phases (thread 0)
-                sub = buf[[3, 20, 21, 22, 23, 4]].astype(np.int64)
-                print(label, "remap sub-phases (us): start, slot0, slots1.., pre-sum, sum+write:",
+                sub = buf[[3, 20, 21, 24, 25, 22, 23, 4]].astype(np.int64)
+                print(label, "remap sub-phases (us): start, slot loads, occupancy, round count, arg-max rounds, "
+                      "pre-sum, sum+write:",
                       np.round(np.diff(sub) / 1e3, 2).tolist(), file=sys.stderr)
             if "--c4" in sys.argv and not warm and buf[12]:  # K0 (router_route_kernel) phases, block (0,0)
                 k0 = buf[8:13].astype(np.int64)
