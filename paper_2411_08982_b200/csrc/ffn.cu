@@ -248,8 +248,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const __grid_consta
       const uint64_t pol_act = policy_evict_last();
       int stage = 0, slot = 0;
       uint32_t phase = 0, uphase = 0;
+      // the first ticket is the CTA's own index (no atomic round trip before
+      // the first load); the counter then hands out tickets from gridDim.x on
+      bool first = true;
       while (true) {
-        int u = atomicAdd(&p.counters[0], 1);
+        int u = first ? static_cast<int>(blockIdx.x) : atomicAdd(&p.counters[0], 1) + static_cast<int>(gridDim.x);
+        first = false;
         if (u >= total) u = -1;
         mbar_wait(&uempty[slot], uphase ^ 1, 1);
         uring[slot] = u;
@@ -508,10 +512,13 @@ __global__ void __launch_bounds__(kPairThreads, 1) ffn_pair_kernel(const __grid_
       const uint64_t pol_act = policy_evict_last();
       int stage = 0, slot = 0;
       uint32_t phase = 0, uphase = 0;
+      bool first = true;  // first ticket = the pair's index, as in ffn_kernel
       while (true) {
         int u;
         if (leader) {
-          u = atomicAdd(&p.counters[0], 1);
+          const int npairs = static_cast<int>(gridDim.x) / 2;
+          u = first ? static_cast<int>(blockIdx.x) / 2 : atomicAdd(&p.counters[0], 1) + npairs;
+          first = false;
           if (u >= total) u = -1;
           mbar_wait(&uempty[slot], uphase ^ 1, 1);
           uring[slot] = u;
